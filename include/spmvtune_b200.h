@@ -1,0 +1,231 @@
+/*
+ * spmvtune_b200.h — C ABI of libspmvtune_b200.so, the B200 (sm_100a) engine
+ * behind the spmvtune drop-in API.
+ *
+ * The reference (`/root/reference/pkg/src/spmvtune`, pure Python/numpy) has
+ * no FFI of its own; every entry point below replaces one reference function
+ * or container operation, cited as file:line relative to that directory.
+ * The Python host package (paper_2411_10143_b200/) binds these with ctypes
+ * (see INTEGRATION.md for the binding a reference maintainer would add).
+ *
+ * Conventions
+ *   - Every function returns an int status (svb_status); nothing throws
+ *     across the ABI.  svb_last_error() returns the calling thread's message
+ *     for the most recent non-zero status.
+ *   - Status -> reference exception (errors.py:4-29):
+ *       SVB_UNSUPPORTED_CONFIG -> UnsupportedConfigError
+ *       SVB_INAPPLICABLE       -> FormatInapplicableError
+ *       SVB_DIM_MISMATCH       -> ValueError
+ *       SVB_NONFINITE          -> SolverNumericalError
+ *       SVB_OOM                -> MemoryError
+ *       SVB_CUDA / SVB_INVALID -> RuntimeError / ValueError
+ *   - Matrices (svb_matrix*) are immutable after creation and may be read
+ *     concurrently from several streams (kernels.py:14-17).  The caller owns
+ *     the handle and releases it with svb_matrix_destroy.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - Pointers named *_dev are device pointers; *_host are host pointers.
+ *   - Index arrays cross the ABI as int64 (the reference's dtype,
+ *     formats.py:34-38); on the device, column indices are int32 and
+ *     row pointers int32 unless nnz >= 2^31 (then int64).
+ */
+#ifndef SPMVTUNE_B200_H
+#define SPMVTUNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVB_ABI_VERSION 1
+
+typedef enum {
+  SVB_OK = 0,
+  SVB_UNSUPPORTED_CONFIG = 1,
+  SVB_INAPPLICABLE = 2,
+  SVB_DIM_MISMATCH = 3,
+  SVB_NONFINITE = 4,
+  SVB_OOM = 5,
+  SVB_CUDA = 6,
+  SVB_INVALID = 7
+} svb_status;
+
+/* FormatTag (formats.py:21-26) */
+typedef enum { SVB_COO = 0, SVB_CSR = 1, SVB_ELL = 2, SVB_DIA = 3, SVB_HYB = 4 } svb_format;
+/* Library (kernels.py:37-40) */
+typedef enum { SVB_LIBA = 0, SVB_LIBB = 1, SVB_LIBC = 2 } svb_library;
+/* value precision of an SpMV call */
+typedef enum { SVB_F64 = 0, SVB_F32 = 1 } svb_dtype;
+
+typedef struct svb_matrix svb_matrix;
+
+typedef struct {
+  int32_t format;        /* svb_format */
+  int32_t ptr64;         /* CSR/COO-derived row pointer is int64 on device */
+  int64_t nrows, ncols;
+  int64_t nnz;           /* stored entries (ELL: non-sentinel cells) */
+  int64_t width;         /* ELL / HYB ELL-part width */
+  int64_t ndiag;         /* DIA */
+  int64_t spill_nnz;     /* HYB COO part */
+  int64_t device_bytes;  /* bytes held on the device by this handle */
+} svb_matrix_info;
+
+/* which host array svb_matrix_download copies out (int64 / float64) */
+typedef enum {
+  SVB_ARR_ROW_PTR = 0,   /* CSR row_ptr, int64[nrows+1] */
+  SVB_ARR_ROWS = 1,      /* COO rows / HYB spill rows, int64[nnz] */
+  SVB_ARR_COLS = 2,      /* CSR/COO cols, int64[nnz]; ELL cols int64[width*nrows] col-major */
+  SVB_ARR_VALS = 3,      /* values, float64 (same layouts) */
+  SVB_ARR_OFFSETS = 4,   /* DIA offsets, int64[ndiag] */
+  SVB_ARR_DATA = 5,      /* DIA data, float64[ndiag*nrows] row-major */
+  SVB_ARR_SPILL_COLS = 6,/* HYB spill cols, int64[spill_nnz] */
+  SVB_ARR_SPILL_VALS = 7 /* HYB spill values, float64[spill_nnz] */
+} svb_array;
+
+/* ---- library ------------------------------------------------------------ */
+const char* svb_last_error(void);
+int svb_abi_version(void);
+/* Select the device for the calling thread and warm the allocator. */
+int svb_init(int device);
+/* Block until `stream` drains (used by host wrappers at API boundaries). */
+int svb_stream_sync(void* stream);
+/* Stream / event / memory plumbing for the host layer (no reference
+ * counterpart: the reference is single-address-space numpy). */
+int svb_stream_create(int priority, void** out);   /* non-blocking stream */
+int svb_stream_destroy(void* stream);
+int svb_event_record(void* stream, void** out);    /* new event, recorded on stream */
+int svb_event_query(void* event);                  /* SVB_OK when complete, else SVB_INVALID */
+int svb_stream_wait_event(void* stream, void* event);
+int svb_event_destroy(void* event);
+int svb_malloc(int64_t bytes, void** out);         /* device memory (pool) */
+int svb_free(void* ptr);
+int svb_host_alloc(int64_t bytes, void** out);     /* pinned host memory */
+int svb_host_free(void* ptr);
+int svb_copy(void* dst, const void* src, int64_t bytes, void* stream);  /* any direction, async */
+int svb_memset(void* dst, int value, int64_t bytes, void* stream);
+int svb_device_info(int32_t* sm_count, int64_t* free_bytes, int64_t* total_bytes);
+
+/* ---- containers (formats.py:50-260) ------------------------------------ */
+/* CooMatrix(nrows, ncols, rows, cols, values): row-major sorted, no dups. */
+int svb_coo_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows_host,
+                   const int64_t* cols_host, const double* vals_host, void* stream,
+                   svb_matrix** out);
+/* CsrMatrix(nrows, ncols, row_ptr, col_idx, values) */
+int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_host,
+                   const int64_t* col_idx_host, const double* vals_host, void* stream,
+                   svb_matrix** out);
+/* EllMatrix(nrows, ncols, width, col_idx, values): column-major (nrows x width)
+ * arrays, i.e. cell (i, k) at k*nrows + i; sentinel column = ncols. */
+int svb_ell_create(int64_t nrows, int64_t ncols, int64_t width, const int64_t* cols_host,
+                   const double* vals_host, void* stream, svb_matrix** out);
+/* DiaMatrix(nrows, ncols, offsets, data): data[k*nrows + i] = A[i, i+offsets[k]] */
+int svb_dia_create(int64_t nrows, int64_t ncols, int64_t ndiag, const int64_t* offsets_host,
+                   const double* data_host, void* stream, svb_matrix** out);
+/* HybMatrix(ell_part, coo_part, split_width): composes copies of two handles */
+int svb_hyb_create(const svb_matrix* ell, const svb_matrix* coo, void* stream,
+                   svb_matrix** out);
+int svb_matrix_destroy(svb_matrix* m);
+int svb_matrix_info_get(const svb_matrix* m, svb_matrix_info* info);
+/* Copy one array back to caller-owned host memory (int64 or float64). */
+int svb_matrix_download(const svb_matrix* m, int which, void* dst_host, void* stream);
+
+/* On-device constant-coefficient stencil generator (configs 1, 2, 5 of
+ * BASELINE.json; no reference counterpart — the reference builds its test
+ * matrices on the host, tests/helpers.py:42-84).  dims[ndim] with the fastest
+ * axis last; offsets[nst*ndim]; weights[nst]. */
+int svb_csr_stencil(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
+                    const double* weights, void* stream, svb_matrix** out);
+
+/* ---- conversion: convert(m, target) (formats.py:302-320) ----------------
+ * Bit-exact with the reference arrays.  DIA above 4096 diagonals returns
+ * SVB_INAPPLICABLE (formats.py:351-356).  `max_ell_cells` (0 = unlimited)
+ * caps nrows*width for ELL (a B200-side memory guard the reference lacks). */
+int svb_convert(const svb_matrix* src, int target, int64_t max_ell_cells, void* stream,
+                svb_matrix** out);
+/* hyb_split_width over the row lengths of m (formats.py:364-370) */
+int svb_hyb_split_width(const svb_matrix* m, void* stream, int64_t* width_out);
+
+/* ---- SpMV: execute_spmv(cfg, m, x, workers=, out=) (kernels.py:274-312) --
+ * y = A x with the (format, library, lane) kernel of the configuration; the
+ * matrix must be stored in `format` (else SVB_UNSUPPORTED_CONFIG, kernels.py:
+ * 125-128).  `workers` is the LibC chunk count (kernels.py:202-248).  All
+ * kernels except COO/LibB reproduce the reference's fp64 summation order
+ * bit-for-bit.  x_dev/y_dev: device vectors of `dtype`. */
+int svb_spmv(const svb_matrix* m, int format, int library, int lane, int workers,
+             int dtype, const void* x_dev, void* y_dev, void* stream);
+/* Same product with host buffers: H2D of x, kernel, D2H of y (the e2e path
+ * of bench.py); staging lives in pinned/device pools owned by the library. */
+int svb_spmv_host(const svb_matrix* m, int format, int library, int lane, int workers,
+                  const double* x_host, double* y_host, void* stream);
+/* spmv_reference(m, x) (formats.py:419-435): sequential row order (CSR). */
+int svb_spmv_sequential(const svb_matrix* csr, const double* x_dev, double* y_dev,
+                        void* stream);
+
+/* ---- features: extract_features(csr) (features.py:68-156) ----------------
+ * agg[7] = {sum r, sum r^2, max r, min r, sum(last-first), sum longest-run,
+ * ndiag}; the host evaluates the 15 float features with the reference's own
+ * expressions (features.py:103-110, 147-150), making them bit-exact. */
+int svb_features(const svb_matrix* csr, int64_t* agg_host, void* stream);
+
+/* ---- Krylov workspaces (solver.py:219-342; CG is new) ---- */
+typedef struct svb_krylov svb_krylov;
+typedef struct {
+  double beta;       /* ||r|| of the last restart/residual call */
+  double hnext;      /* ||w|| after MGS (GMRES) */
+  double estimate;   /* |g[j+1]|/||b|| (GMRES) or ||r||/||b|| (CG) */
+  double hjj;        /* rotated H[j,j] (GMRES breakdown check) */
+  double pq;         /* p.Ap (CG) */
+  int32_t nonfinite; /* a non-finite scalar was produced */
+  int32_t pad;
+} svb_krylov_status;
+
+/* n rows, restart m (GMRES; m = 0 for CG).  Owns V[(m+1) x n], H, Givens
+ * state, CG vectors and the mapped status block. */
+int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out);
+int svb_krylov_destroy(svb_krylov* k);
+/* device pointers of workspace vectors: 0..m = V rows; -1 = x; -2 = b;
+ * -3 = tmp (matvec target); -4 = CG p; -5 = CG q; -6 = CG r */
+int svb_krylov_vec(svb_krylov* k, int which, double** out);
+int svb_krylov_status_get(svb_krylov* k, void* stream, svb_krylov_status* out);
+/* ||b|| into status.beta */
+int svb_krylov_bnorm(svb_krylov* k, void* stream);
+/* GMRES cycle start: r = b - tmp; beta = ||r||; V0 = r/beta; g = beta e1 */
+int svb_gmres_restart(svb_krylov* k, void* stream);
+/* GMRES Arnoldi step j after the matvec wrote V[j+1] = A V[j]: fused
+ * modified Gram-Schmidt (axpy_i + dot_{i+1} per pass), ||w||, Givens
+ * rotations and the residual estimate, all on device. */
+int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream);
+/* V[j+1] /= hnext */
+int svb_gmres_normalize(svb_krylov* k, int32_t j, void* stream);
+/* x += V[:j+1]^T y with y from the rotated triangular system (solver.py:211-216) */
+int svb_gmres_update_x(svb_krylov* k, int32_t j, void* stream);
+/* status.beta = ||b - tmp|| (explicit residual confirmation) */
+int svb_krylov_residual(svb_krylov* k, void* stream);
+/* CG: r = b - tmp, p = r, rr = r.r  (tmp = A x) */
+int svb_cg_restart(svb_krylov* k, void* stream);
+/* CG after q = A p: alpha = rr/(p.q); x += alpha p; r -= alpha q; rr' = r.r;
+ * estimate = sqrt(rr')/bnorm; p = r + (rr'/rr) p */
+int svb_cg_step(svb_krylov* k, double bnorm, void* stream);
+
+/* ---- generic fused vector ops (device vectors of length n) -------------- */
+int svb_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host,
+            void* stream);
+
+/* ---- compiled cascade inference (inference.py:55-125, model_schema.md) ---
+ * Flattened tree ensemble: node arrays in the reference's flattening order;
+ * leaves carry feature = -1.  Evaluation: `<=` goes left, per-class sums in
+ * list order as float64, argmax ties to the lowest index. */
+typedef struct svb_forest svb_forest;
+int svb_forest_create(int32_t nclasses, int32_t ntrees, const int32_t* tree_class,
+                      const int32_t* roots, int32_t nnodes, const int32_t* feature,
+                      const double* threshold, const int32_t* left, const int32_t* right,
+                      const double* score, svb_forest** out);
+int svb_forest_destroy(svb_forest* f);
+int svb_forest_predict(const svb_forest* f, const double* x15, double* scores_out,
+                       int32_t* label_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMVTUNE_B200_H */

@@ -1,0 +1,167 @@
+"""ctypes binding of libspmvtune_b200.so (the C ABI in include/spmvtune_b200.h).
+
+Loading is lazy but loud: every product entry point goes through ``lib()``,
+which raises ImportError if the in-tree library was not built.  There is no
+CPU fallback anywhere in the package.  Non-zero statuses map onto the
+reference's exception hierarchy (errors.py:4-29) via ``check``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import (FormatInapplicableError, SolverNumericalError,
+                     UnsupportedConfigError)
+
+LIB_PATH = Path(__file__).resolve().parent / "libspmvtune_b200.so"
+
+OK, UNSUPPORTED, INAPPLICABLE, DIM_MISMATCH, NONFINITE, OOM, CUDA, INVALID = range(8)
+COO, CSR, ELL, DIA, HYB = range(5)
+LIBA, LIBB, LIBC = range(3)
+F64, F32 = 0, 1
+ARR_ROW_PTR, ARR_ROWS, ARR_COLS, ARR_VALS, ARR_OFFSETS, ARR_DATA, ARR_SPILL_COLS, ARR_SPILL_VALS = range(8)
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_D = C.c_double
+_PI64 = C.POINTER(C.c_int64)
+_PD = C.POINTER(C.c_double)
+_PP = C.POINTER(C.c_void_p)
+
+
+class MatrixInfo(C.Structure):
+    _fields_ = [("format", C.c_int32), ("ptr64", C.c_int32), ("nrows", C.c_int64),
+                ("ncols", C.c_int64), ("nnz", C.c_int64), ("width", C.c_int64),
+                ("ndiag", C.c_int64), ("spill_nnz", C.c_int64), ("device_bytes", C.c_int64)]
+
+
+class KrylovStatus(C.Structure):
+    _fields_ = [("beta", C.c_double), ("hnext", C.c_double), ("estimate", C.c_double),
+                ("hjj", C.c_double), ("pq", C.c_double), ("nonfinite", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+# name -> argtypes (all functions return int status unless listed in _RESTYPE)
+_SIGS = {
+    "svb_last_error": [],
+    "svb_abi_version": [],
+    "svb_init": [C.c_int],
+    "svb_stream_sync": [_P],
+    "svb_stream_create": [C.c_int, _PP],
+    "svb_stream_destroy": [_P],
+    "svb_event_record": [_P, _PP],
+    "svb_event_query": [_P],
+    "svb_stream_wait_event": [_P, _P],
+    "svb_event_destroy": [_P],
+    "svb_malloc": [_I64, _PP],
+    "svb_free": [_P],
+    "svb_host_alloc": [_I64, _PP],
+    "svb_host_free": [_P],
+    "svb_copy": [_P, _P, _I64, _P],
+    "svb_memset": [_P, C.c_int, _I64, _P],
+    "svb_device_info": [C.POINTER(C.c_int32), _PI64, _PI64],
+    "svb_coo_create": [_I64, _I64, _I64, _P, _P, _P, _P, _PP],
+    "svb_csr_create": [_I64, _I64, _I64, _P, _P, _P, _P, _PP],
+    "svb_ell_create": [_I64, _I64, _I64, _P, _P, _P, _PP],
+    "svb_dia_create": [_I64, _I64, _I64, _P, _P, _P, _PP],
+    "svb_hyb_create": [_P, _P, _P, _PP],
+    "svb_matrix_destroy": [_P],
+    "svb_matrix_info_get": [_P, C.POINTER(MatrixInfo)],
+    "svb_matrix_download": [_P, C.c_int, _P, _P],
+    "svb_csr_stencil": [C.c_int, _PI64, C.c_int, C.POINTER(C.c_int32), _PD, _P, _PP],
+    "svb_convert": [_P, C.c_int, _I64, _P, _PP],
+    "svb_hyb_split_width": [_P, _P, _PI64],
+    "svb_spmv": [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P],
+    "svb_spmv_host": [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P],
+    "svb_spmv_sequential": [_P, _P, _P, _P],
+    "svb_features": [_P, _PI64, _P],
+    "svb_krylov_create": [_I64, _I32, _PP],
+    "svb_krylov_destroy": [_P],
+    "svb_krylov_vec": [_P, C.c_int, _PP],
+    "svb_krylov_status_get": [_P, _P, C.POINTER(KrylovStatus)],
+    "svb_krylov_bnorm": [_P, _P],
+    "svb_krylov_residual": [_P, _P],
+    "svb_gmres_restart": [_P, _P],
+    "svb_gmres_arnoldi": [_P, _I32, _D, _P],
+    "svb_gmres_normalize": [_P, _I32, _P],
+    "svb_gmres_update_x": [_P, _I32, _P],
+    "svb_cg_restart": [_P, _P],
+    "svb_cg_step": [_P, _D, _P],
+    "svb_dot": [_P, _P, _I64, _PD, _P],
+    "svb_forest_create": [_I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _PP],
+    "svb_forest_destroy": [_P],
+    "svb_forest_predict": [_P, _P, _P, _P],
+}
+_RESTYPE = {"svb_last_error": C.c_char_p}
+
+_lock = threading.Lock()
+_lib = None
+_initialised = False
+
+
+def exported_symbols():
+    """Names the header declares (checked against the .so by the CPU tests)."""
+    return sorted(_SIGS)
+
+
+def load():
+    """dlopen the library and bind signatures (no CUDA call is made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH.name} is not built; run `python -m paper_2411_10143_b200.build` "
+                    "(this package has no CPU fallback)")
+            lib_ = C.CDLL(str(LIB_PATH))
+            for name, args in _SIGS.items():
+                fn = getattr(lib_, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPE.get(name, C.c_int)
+            _lib = lib_
+    return _lib
+
+
+def lib():
+    """The library, with the CUDA device selected for the calling process."""
+    global _initialised
+    L = load()
+    if not _initialised:
+        with _lock:
+            if not _initialised:
+                dev = int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("SPMVTUNE_DEVICE") is None \
+                    else int(os.environ["SPMVTUNE_DEVICE"])
+                check(L.svb_init(dev))
+                _initialised = True
+    return L
+
+
+def last_error() -> str:
+    raw = load().svb_last_error()
+    return raw.decode("utf-8", "replace") if raw else ""
+
+
+_EXC = {UNSUPPORTED: UnsupportedConfigError, INAPPLICABLE: FormatInapplicableError,
+        DIM_MISMATCH: ValueError, NONFINITE: SolverNumericalError, OOM: MemoryError,
+        CUDA: RuntimeError, INVALID: ValueError}
+
+
+def check(status: int) -> None:
+    if status != OK:
+        raise _EXC.get(status, RuntimeError)(last_error() or f"spmvtune_b200 status {status}")
+
+
+def ptr(a) -> int:
+    """Raw address of a numpy array / torch tensor / int."""
+    if a is None:
+        return 0
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return int(a.data_ptr())
+    return int(a.ctypes.data)

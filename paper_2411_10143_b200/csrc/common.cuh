@@ -1,0 +1,211 @@
+// Shared device/host plumbing for libspmvtune_b200 (sm_100a).
+//
+// Status codes, the thread-local error string behind svb_last_error(), the
+// stream-ordered device allocator wrapper, grid sizing for the 148-SM B200,
+// and the fp summation-order primitives every "exact" kernel uses
+// (numpy's pairwise sum).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <memory>
+#include <string>
+
+#include "../../include/spmvtune_b200.h"
+
+namespace svb {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define SVB_CUDA_TRY(expr)                                                   \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      throw ::svb::Error{_e == cudaErrorMemoryAllocation ? SVB_OOM : SVB_CUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+    }                                                                        \
+  } while (0)
+
+#define SVB_CHECK_LAUNCH() SVB_CUDA_TRY(cudaGetLastError())
+
+#define SVB_REQUIRE(cond, code, msg)                \
+  do {                                                \
+    if (!(cond)) throw ::svb::Error{(code), (msg)};   \
+  } while (0)
+
+// Runs `body` and maps exceptions onto status codes (never throws across
+// the C ABI).
+template <class F>
+int guard(F&& body) {
+  try {
+    body();
+    return SVB_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return SVB_OOM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return SVB_INVALID;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// device memory: stream-ordered pool allocations, shared between immutable
+// matrix handles (a CSR->COO conversion shares col/val buffers, for example)
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = 0;  // freed stream-ordered on the allocating stream
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+};
+using Buf = std::shared_ptr<DevBuf>;
+
+Buf alloc(size_t bytes, cudaStream_t s);
+
+template <class T>
+inline T* ptr(const Buf& b) {
+  return b ? static_cast<T*>(b->ptr) : nullptr;
+}
+
+int sm_count();
+
+// Grid for a grid-stride streaming kernel: enough CTAs to cover the work,
+// capped at `per_sm` resident CTAs on every SM.
+inline unsigned grid_for(int64_t work_items, int block, int per_sm = 8) {
+  int64_t need = (work_items + block - 1) / block;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need < 1) need = 1;
+  return (unsigned)(need < cap ? need : cap);
+}
+
+// ---------------------------------------------------------------------------
+// summation-order primitives (numpy pairwise sum)
+// ---------------------------------------------------------------------------
+// numpy pairwise leaf (n <= 128): 8 strided accumulators, fixed combine tree,
+// sequential tail.  `get(i)` yields the i-th addend.
+template <class T, class G>
+__device__ __forceinline__ T pw_leaf(const G& get, int64_t lo, int64_t n) {
+  if (n < 8) {
+    T r = T(-0.0);
+    for (int64_t i = 0; i < n; ++i) r = r + get(lo + i);
+    return r;
+  }
+  T r0 = get(lo + 0), r1 = get(lo + 1), r2 = get(lo + 2), r3 = get(lo + 3);
+  T r4 = get(lo + 4), r5 = get(lo + 5), r6 = get(lo + 6), r7 = get(lo + 7);
+  const int64_t lim = n - (n % 8);
+  int64_t i = 8;
+  for (; i < lim; i += 8) {
+    r0 = r0 + get(lo + i + 0);
+    r1 = r1 + get(lo + i + 1);
+    r2 = r2 + get(lo + i + 2);
+    r3 = r3 + get(lo + i + 3);
+    r4 = r4 + get(lo + i + 4);
+    r5 = r5 + get(lo + i + 5);
+    r6 = r6 + get(lo + i + 6);
+    r7 = r7 + get(lo + i + 7);
+  }
+  T res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res = res + get(lo + i);
+  return res;
+}
+
+// Full numpy pairwise sum: n <= 128 is a leaf, otherwise split at
+// n2 = n/2 rounded down to a multiple of 8 and add the halves.  The
+// recursion is unrolled onto an explicit stack (depth <= 28 covers 2^31
+// addends) so the common short-segment path carries no call frames.
+template <class T, class G>
+__device__ T pw_sum(const G& get, int64_t lo, int64_t n) {
+  if (n <= 128) return pw_leaf<T>(get, lo, n);
+  struct Frame {
+    int64_t lo, n;
+    T left;
+    int state;
+  };
+  Frame st[28];
+  int sp = 0;
+  st[0] = {lo, n, T(0), 0};
+  T ret = T(0);
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      ret = pw_leaf<T>(get, f.lo, f.n);
+      --sp;
+      continue;
+    }
+    int64_t n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[sp + 1] = {f.lo, n2, T(0), 0};
+      ++sp;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.lo + n2, f.n - n2, T(0), 0};
+      ++sp;
+    } else {
+      ret = f.left + ret;
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// One np.add.reduceat segment [s, e), e > s: p[s] + pairwise(p[s+1:e]).
+template <class T, class G>
+__device__ __forceinline__ T segment_sum(const G& get, int64_t s, int64_t e) {
+  T head = get(s);
+  if (e - s == 1) return head;
+  return head + pw_sum<T>(get, s + 1, e - s - 1);
+}
+
+// ---------------------------------------------------------------------------
+// cache-hinted loads: streamed matrix arrays bypass L1 allocation, the
+// gathered x vector uses the read-only path and stays cached
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ long long ld_stream(const long long* p) {
+  long long v;
+  asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+template <class T>
+__device__ __forceinline__ T ld_x(const T* p) {
+  return __ldg(p);
+}
+
+}  // namespace svb

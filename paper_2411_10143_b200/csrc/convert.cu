@@ -1,0 +1,499 @@
+// Format conversion on the device: convert(m, target) (formats.py:302-320).
+//
+// The reference routes every conversion through COO (to_coo, formats.py:
+// 281-299).  Here every source is first reduced to a "row view" — an int64
+// row pointer plus int32 columns and f64 values in row-major order — which
+// CSR and COO sources provide without copying; ELL/DIA/HYB sources are
+// expanded by a count -> scan -> fill pass.  Targets are then built from the
+// row view.  All index/value arrays are bit-identical to the reference's.
+#include <algorithm>
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace svb {
+
+struct RowView {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  Buf ptr;   // int64 [nrows+1]
+  Buf rows;  // int32 [nnz] (only when already available)
+  Buf cols;  // int32 [nnz]
+  Buf vals;  // f64 [nnz]
+};
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------------------
+// to row view from ELL / DIA / HYB
+// ---------------------------------------------------------------------------
+__global__ void k_ell_count(int64_t nrows, int64_t ncols, int64_t width, const int* __restrict__ cols,
+                            int64_t* __restrict__ cnt) {
+  GRID_STRIDE(i, nrows) {
+    int64_t c = 0;
+    for (int64_t k = 0; k < width; ++k) c += cols[k * nrows + i] != ncols;
+    cnt[i] = c;
+  }
+}
+
+__global__ void k_ell_fill(int64_t nrows, int64_t ncols, int64_t width, const int* __restrict__ ecols,
+                           const double* __restrict__ evals, const int64_t* __restrict__ ptr,
+                           int* __restrict__ cols, double* __restrict__ vals) {
+  GRID_STRIDE(i, nrows) {
+    int64_t o = ptr[i];
+    for (int64_t k = 0; k < width; ++k) {
+      const int c = ecols[k * nrows + i];
+      if (c != ncols) {
+        cols[o] = c;
+        vals[o] = evals[k * nrows + i];
+        ++o;
+      }
+    }
+  }
+}
+
+__global__ void k_dia_count(int64_t nrows, int64_t ncols, int64_t ndiag, const long long* __restrict__ offs,
+                            const double* __restrict__ data, int64_t* __restrict__ cnt) {
+  GRID_STRIDE(i, nrows) {
+    int64_t c = 0;
+    for (int64_t k = 0; k < ndiag; ++k) {
+      const int64_t j = i + offs[k];
+      c += (j >= 0 && j < ncols && data[k * nrows + i] != 0.0);
+    }
+    cnt[i] = c;
+  }
+}
+
+__global__ void k_dia_fill(int64_t nrows, int64_t ncols, int64_t ndiag, const long long* __restrict__ offs,
+                           const double* __restrict__ data, const int64_t* __restrict__ ptr,
+                           int* __restrict__ cols, double* __restrict__ vals) {
+  GRID_STRIDE(i, nrows) {
+    int64_t o = ptr[i];
+    for (int64_t k = 0; k < ndiag; ++k) {
+      const int64_t j = i + offs[k];
+      const double v = data[k * nrows + i];
+      if (j >= 0 && j < ncols && v != 0.0) {
+        cols[o] = (int)j;
+        vals[o] = v;
+        ++o;
+      }
+    }
+  }
+}
+
+// HYB -> row view: merge the row's ELL cells (k order) with its spill run,
+// by column, as from_triplets' lexsort would (formats.py:292-298).
+__global__ void k_hyb_count(int64_t nrows, int64_t ncols, int64_t width, const int* __restrict__ ecols,
+                            const int64_t* __restrict__ sptr, int64_t* __restrict__ cnt) {
+  GRID_STRIDE(i, nrows) {
+    int64_t c = sptr[i + 1] - sptr[i];
+    for (int64_t k = 0; k < width; ++k) c += ecols[k * nrows + i] != ncols;
+    cnt[i] = c;
+  }
+}
+
+__global__ void k_hyb_fill(int64_t nrows, int64_t ncols, int64_t width, const int* __restrict__ ecols,
+                           const double* __restrict__ evals, const int64_t* __restrict__ sptr,
+                           const int* __restrict__ scols, const double* __restrict__ svals,
+                           const int64_t* __restrict__ ptr, int* __restrict__ cols,
+                           double* __restrict__ vals) {
+  GRID_STRIDE(i, nrows) {
+    int64_t o = ptr[i];
+    int64_t k = 0, q = sptr[i];
+    const int64_t qe = sptr[i + 1];
+    // advance k to the next stored ELL cell
+    auto next_k = [&](int64_t kk) {
+      while (kk < width && ecols[kk * nrows + i] == ncols) ++kk;
+      return kk;
+    };
+    k = next_k(0);
+    while (k < width || q < qe) {
+      const bool take_ell = q >= qe || (k < width && ecols[k * nrows + i] < scols[q]);
+      if (take_ell) {
+        cols[o] = ecols[k * nrows + i];
+        vals[o] = evals[k * nrows + i];
+        k = next_k(k + 1);
+      } else {
+        cols[o] = scols[q];
+        vals[o] = svals[q];
+        ++q;
+      }
+      ++o;
+    }
+  }
+}
+
+static RowView row_view(const svb_matrix* m, cudaStream_t s) {
+  RowView v;
+  v.nrows = m->nrows;
+  v.ncols = m->ncols;
+  const int64_t n = m->nrows;
+  if (m->fmt == SVB_CSR) {
+    v.nnz = m->nnz;
+    v.ptr = alloc((n + 1) * 8, s);
+    ptr_to_i64(m, ptr<int64_t>(v.ptr), s);
+    v.cols = m->cols;
+    v.vals = m->vals;
+    return v;
+  }
+  if (m->fmt == SVB_COO) {
+    v.nnz = m->nnz;
+    v.ptr = rows_to_ptr(ptr<int32_t>(m->rows), m->nnz, n, true, s);
+    v.rows = m->rows;
+    v.cols = m->cols;
+    v.vals = m->vals;
+    return v;
+  }
+  Buf cnt = alloc(n * 8, s);
+  const unsigned g = grid_for(n, 256);
+  if (m->fmt == SVB_ELL)
+    k_ell_count<<<g, 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), ptr<int64_t>(cnt));
+  else if (m->fmt == SVB_DIA)
+    k_dia_count<<<g, 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), ptr<double>(m->vals),
+                                  ptr<int64_t>(cnt));
+  else
+    k_hyb_count<<<g, 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), ptr<int64_t>(m->ptr),
+                                  ptr<int64_t>(cnt));
+  SVB_CHECK_LAUNCH();
+  v.ptr = alloc((n + 1) * 8, s);
+  v.nnz = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(v.ptr), n, s);
+  v.cols = alloc(v.nnz * 4, s);
+  v.vals = alloc(v.nnz * 8, s);
+  if (m->fmt == SVB_ELL)
+    k_ell_fill<<<g, 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), ptr<double>(m->vals),
+                                 ptr<int64_t>(v.ptr), ptr<int>(v.cols), ptr<double>(v.vals));
+  else if (m->fmt == SVB_DIA)
+    k_dia_fill<<<g, 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), ptr<double>(m->vals),
+                                 ptr<int64_t>(v.ptr), ptr<int>(v.cols), ptr<double>(v.vals));
+  else
+    k_hyb_fill<<<g, 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), ptr<double>(m->vals),
+                                 ptr<int64_t>(m->ptr), ptr<int>(m->scols), ptr<double>(m->svals),
+                                 ptr<int64_t>(v.ptr), ptr<int>(v.cols), ptr<double>(v.vals));
+  SVB_CHECK_LAUNCH();
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// row statistics used by the builders
+// ---------------------------------------------------------------------------
+__global__ void k_max_len(int64_t nrows, const int64_t* __restrict__ ptr, unsigned long long* out) {
+  int64_t best = 0;
+  GRID_STRIDE(i, nrows) best = max(best, ptr[i + 1] - ptr[i]);
+  for (int o = 16; o; o >>= 1) best = max(best, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)best);
+}
+
+static int64_t max_row_len(const RowView& v, cudaStream_t s) {
+  Buf d = alloc(8, s);
+  SVB_CUDA_TRY(cudaMemsetAsync(d->ptr, 0, 8, s));
+  k_max_len<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, ptr<int64_t>(v.ptr),
+                                                   ptr<unsigned long long>(d));
+  SVB_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  SVB_CUDA_TRY(cudaMemcpyAsync(&h, d->ptr, 8, cudaMemcpyDeviceToHost, s));
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  return (int64_t)h;
+}
+
+// row-length histogram, privatised in shared memory for short lengths
+constexpr int HIST_SMEM = 4096;
+__global__ void k_len_hist(int64_t nrows, const int64_t* __restrict__ ptr, int64_t nbins,
+                           unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int sh[HIST_SMEM];
+  const int64_t local = nbins < HIST_SMEM ? nbins : HIST_SMEM;
+  for (int b = threadIdx.x; b < local; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  GRID_STRIDE(i, nrows) {
+    const int64_t L = ptr[i + 1] - ptr[i];
+    if (L < HIST_SMEM) atomicAdd(sh + L, 1u);
+    else atomicAdd(hist + L, 1ull);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < local; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, (unsigned long long)sh[b]);
+}
+
+// hyb_split_width (formats.py:364-370): sorted(lens)[ceil(2n/3) - 1] from the
+// histogram's cumulative counts
+static int64_t hyb_width(const RowView& v, int64_t maxlen, cudaStream_t s) {
+  const int64_t n = v.nrows;
+  if (n == 0) return 0;
+  const int64_t nbins = maxlen + 1;
+  Buf h = alloc(nbins * 8, s);
+  SVB_CUDA_TRY(cudaMemsetAsync(h->ptr, 0, nbins * 8, s));
+  k_len_hist<<<grid_for(n, 256, 4), 256, 0, s>>>(n, ptr<int64_t>(v.ptr), nbins,
+                                                ptr<unsigned long long>(h));
+  SVB_CHECK_LAUNCH();
+  std::vector<unsigned long long> hh(nbins);
+  SVB_CUDA_TRY(cudaMemcpyAsync(hh.data(), h->ptr, nbins * 8, cudaMemcpyDeviceToHost, s));
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t need = (2 * n + 2) / 3;  // ceil(2n/3)
+  int64_t cum = 0;
+  for (int64_t L = 0; L < nbins; ++L) {
+    cum += (int64_t)hh[L];
+    if (cum >= need) return L;
+  }
+  return maxlen;
+}
+
+// ---------------------------------------------------------------------------
+// builders
+// ---------------------------------------------------------------------------
+// ELL(width) cells from the first min(len, width) entries of every row;
+// column-major, sentinel col = ncols / value 0 (formats.py:339-348, 379-385)
+__global__ void k_to_ell(int64_t nrows, int64_t ncols, int64_t width, const int64_t* __restrict__ ptr,
+                         const int* __restrict__ cols, const double* __restrict__ vals,
+                         int* __restrict__ ecols, double* __restrict__ evals) {
+  GRID_STRIDE(i, nrows) {
+    const int64_t s = ptr[i], len = ptr[i + 1] - s;
+    for (int64_t k = 0; k < width; ++k) {
+      const bool has = k < len;
+      ecols[k * nrows + i] = has ? cols[s + k] : (int)ncols;
+      evals[k * nrows + i] = has ? vals[s + k] : 0.0;
+    }
+  }
+}
+
+__global__ void k_spill_count(int64_t nrows, int64_t width, const int64_t* __restrict__ ptr,
+                              int64_t* __restrict__ cnt) {
+  GRID_STRIDE(i, nrows) { const int64_t d = ptr[i + 1] - ptr[i] - width; cnt[i] = d > 0 ? d : 0; }
+}
+
+__global__ void k_spill_fill(int64_t nrows, int64_t width, const int64_t* __restrict__ ptr,
+                             const int* __restrict__ cols, const double* __restrict__ vals,
+                             const int64_t* __restrict__ sptr, int* __restrict__ srows,
+                             int* __restrict__ scols, double* __restrict__ svals) {
+  GRID_STRIDE(i, nrows) {
+    int64_t o = sptr[i];
+    for (int64_t k = ptr[i] + width; k < ptr[i + 1]; ++k, ++o) {
+      srows[o] = (int)i;
+      scols[o] = cols[k];
+      svals[o] = vals[k];
+    }
+  }
+}
+
+// diagonal occupancy bitmap: bit (col - row + nrows - 1); test before the
+// atomic so the hot diagonals of banded matrices are not contended
+__global__ void k_diag_bits(int64_t nrows, const int64_t* __restrict__ ptr, const int* __restrict__ cols,
+                            unsigned* __restrict__ bits) {
+  GRID_STRIDE(i, nrows) {
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+      const int64_t d = (int64_t)cols[k] - i + nrows - 1;
+      const unsigned m = 1u << (d & 31);
+      unsigned* w = bits + (d >> 5);
+      if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+    }
+  }
+}
+
+__global__ void k_popc(int64_t nwords, const unsigned* __restrict__ bits, int64_t* __restrict__ cnt) {
+  GRID_STRIDE(w, nwords) cnt[w] = __popc(bits[w]);
+}
+
+__global__ void k_bits_to_offsets(int64_t nwords, int64_t nrows, const unsigned* __restrict__ bits,
+                                  const int64_t* __restrict__ pos, long long* __restrict__ offs) {
+  GRID_STRIDE(w, nwords) {
+    unsigned b = bits[w];
+    int64_t o = pos[w];
+    while (b) {
+      const int t = __ffs(b) - 1;
+      offs[o++] = w * 32 + t - (nrows - 1);
+      b &= b - 1;
+    }
+  }
+}
+
+constexpr int DIA_CAP = 4096;  // DIA_OFFSET_CAP (formats.py:18)
+
+__global__ void k_dia_scatter(int64_t nrows, int64_t ndiag, const long long* __restrict__ offs,
+                              const int64_t* __restrict__ ptr, const int* __restrict__ cols,
+                              const double* __restrict__ vals, double* __restrict__ data) {
+  __shared__ long long so[DIA_CAP];
+  for (int k = threadIdx.x; k < ndiag; k += blockDim.x) so[k] = offs[k];
+  __syncthreads();
+  GRID_STRIDE(i, nrows) {
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+      const long long d = (long long)cols[e] - i;
+      int lo = 0, hi = (int)ndiag;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (so[mid] < d) lo = mid + 1; else hi = mid;
+      }
+      data[(int64_t)lo * nrows + i] = vals[e];
+    }
+  }
+}
+
+static svb_matrix* new_like(const RowView& v, int fmt) {
+  auto m = new svb_matrix();
+  m->fmt = fmt;
+  m->nrows = v.nrows;
+  m->ncols = v.ncols;
+  m->nnz = v.nnz;
+  return m;
+}
+
+static svb_matrix* build_csr(const RowView& v, cudaStream_t s) {
+  auto m = new_like(v, SVB_CSR);
+  m->ptr64 = v.nnz >= INT32_MAX;
+  if (m->ptr64) m->ptr = v.ptr;
+  else {
+    m->ptr = alloc((v.nrows + 1) * 4, s);
+    narrow_i64_to_i32(ptr<int64_t>(v.ptr), ptr<int32_t>(m->ptr), v.nrows + 1, s);
+  }
+  m->cols = v.cols;
+  m->vals = v.vals;
+  return m;
+}
+
+static svb_matrix* build_coo(const RowView& v, const svb_matrix* src, cudaStream_t s) {
+  auto m = new_like(v, SVB_COO);
+  m->ptr64 = v.nnz >= INT32_MAX;
+  if (v.rows) m->rows = v.rows;
+  else {
+    svb_matrix tmp;  // CSR-shaped view over the row pointer for the expansion kernel
+    tmp.nrows = v.nrows;
+    tmp.nnz = v.nnz;
+    tmp.ptr64 = true;
+    tmp.ptr = v.ptr;
+    m->rows = ptr_to_rows(&tmp, s);
+  }
+  m->cols = v.cols;
+  m->vals = v.vals;
+  (void)src;
+  return m;
+}
+
+static svb_matrix* build_ell(const RowView& v, int64_t max_cells, cudaStream_t s) {
+  const int64_t width = v.nnz ? max_row_len(v, s) : 0;
+  if (max_cells > 0 && width > 0 && width > max_cells / std::max<int64_t>(v.nrows, 1))
+    throw Error{SVB_INAPPLICABLE, "ELL would need " + std::to_string(v.nrows) + " x " +
+                                      std::to_string(width) + " cells, above the device cap of " +
+                                      std::to_string(max_cells) + "; ELL is inapplicable"};
+  auto m = new_like(v, SVB_ELL);
+  m->width = width;
+  m->cols = alloc(width * v.nrows * 4, s);
+  m->vals = alloc(width * v.nrows * 8, s);
+  if (width) {
+    k_to_ell<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, v.ncols, width, ptr<int64_t>(v.ptr),
+                                                    ptr<int>(v.cols), ptr<double>(v.vals), ptr<int>(m->cols),
+                                                    ptr<double>(m->vals));
+    SVB_CHECK_LAUNCH();
+  }
+  return m;
+}
+
+static svb_matrix* build_dia(const RowView& v, cudaStream_t s) {
+  const int64_t nbits = v.nrows + v.ncols - 1;
+  const int64_t nwords = (nbits + 31) / 32;
+  Buf bits = alloc(nwords * 4, s);
+  SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
+  if (v.nnz) {
+    k_diag_bits<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+                                                       ptr<unsigned>(bits));
+    SVB_CHECK_LAUNCH();
+  }
+  Buf cnt = alloc(nwords * 8, s);
+  k_popc<<<grid_for(nwords, 256), 256, 0, s>>>(nwords, ptr<unsigned>(bits), ptr<int64_t>(cnt));
+  SVB_CHECK_LAUNCH();
+  Buf pos = alloc((nwords + 1) * 8, s);
+  const int64_t ndiag = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(pos), nwords, s);
+  if (ndiag > DIA_CAP)
+    throw Error{SVB_INAPPLICABLE, "matrix populates " + std::to_string(ndiag) +
+                                      " diagonals, above the cap of " + std::to_string(DIA_CAP) +
+                                      "; DIA is inapplicable"};
+  auto m = new_like(v, SVB_DIA);
+  m->ndiag = ndiag;
+  m->offs = alloc(ndiag * 8, s);
+  m->vals = alloc(ndiag * v.nrows * 8, s);
+  if (ndiag) {
+    k_bits_to_offsets<<<grid_for(nwords, 256), 256, 0, s>>>(nwords, v.nrows, ptr<unsigned>(bits),
+                                                            ptr<int64_t>(pos), ptr<long long>(m->offs));
+    SVB_CHECK_LAUNCH();
+    SVB_CUDA_TRY(cudaMemsetAsync(m->vals->ptr, 0, ndiag * v.nrows * 8, s));
+    k_dia_scatter<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, ndiag, ptr<long long>(m->offs),
+                                                         ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+                                                         ptr<double>(v.vals), ptr<double>(m->vals));
+    SVB_CHECK_LAUNCH();
+    m->h_offs.resize(ndiag);
+    SVB_CUDA_TRY(cudaMemcpyAsync(m->h_offs.data(), m->offs->ptr, ndiag * 8, cudaMemcpyDeviceToHost, s));
+  }
+  // DiaMatrix keeps no nnz; report the stored (in-range) cells like svb_dia_create
+  int64_t stored = 0;
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int64_t k = 0; k < ndiag; ++k) {
+    const int64_t off = m->h_offs[k];
+    const int64_t lo = off < 0 ? -off : 0, hi = std::min<int64_t>(v.nrows, v.ncols - off);
+    if (hi > lo) stored += hi - lo;
+  }
+  m->nnz = stored;
+  return m;
+}
+
+static svb_matrix* build_hyb(const RowView& v, cudaStream_t s) {
+  const int64_t maxlen = v.nnz ? max_row_len(v, s) : 0;
+  const int64_t w = hyb_width(v, maxlen, s);
+  auto m = new_like(v, SVB_HYB);
+  m->width = w;
+  m->cols = alloc(w * v.nrows * 4, s);
+  m->vals = alloc(w * v.nrows * 8, s);
+  const unsigned g = grid_for(v.nrows, 256);
+  if (w) {
+    k_to_ell<<<g, 256, 0, s>>>(v.nrows, v.ncols, w, ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+                               ptr<double>(v.vals), ptr<int>(m->cols), ptr<double>(m->vals));
+    SVB_CHECK_LAUNCH();
+  }
+  Buf cnt = alloc(v.nrows * 8, s);
+  k_spill_count<<<g, 256, 0, s>>>(v.nrows, w, ptr<int64_t>(v.ptr), ptr<int64_t>(cnt));
+  SVB_CHECK_LAUNCH();
+  m->ptr = alloc((v.nrows + 1) * 8, s);
+  m->spill_nnz = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(m->ptr), v.nrows, s);
+  m->rows = alloc(m->spill_nnz * 4, s);
+  m->scols = alloc(m->spill_nnz * 4, s);
+  m->svals = alloc(m->spill_nnz * 8, s);
+  if (m->spill_nnz) {
+    k_spill_fill<<<g, 256, 0, s>>>(v.nrows, w, ptr<int64_t>(v.ptr), ptr<int>(v.cols), ptr<double>(v.vals),
+                                   ptr<int64_t>(m->ptr), ptr<int>(m->rows), ptr<int>(m->scols),
+                                   ptr<double>(m->svals));
+    SVB_CHECK_LAUNCH();
+  }
+  return m;
+}
+
+}  // namespace svb
+
+using namespace svb;
+
+extern "C" {
+
+int svb_convert(const svb_matrix* src, int target, int64_t max_ell_cells, void* stream,
+                svb_matrix** out) {
+  return guard([&] {
+    SVB_REQUIRE(src && out, SVB_INVALID, "null handle");
+    SVB_REQUIRE(target >= SVB_COO && target <= SVB_HYB, SVB_INVALID, "unknown format tag");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    RowView v = row_view(src, s);
+    svb_matrix* m = nullptr;
+    switch (target) {
+      case SVB_COO: m = build_coo(v, src, s); break;
+      case SVB_CSR: m = build_csr(v, s); break;
+      case SVB_ELL: m = build_ell(v, max_ell_cells, s); break;
+      case SVB_DIA: m = build_dia(v, s); break;
+      default: m = build_hyb(v, s); break;
+    }
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_hyb_split_width(const svb_matrix* m, void* stream, int64_t* width_out) {
+  return guard([&] {
+    SVB_REQUIRE(m && width_out, SVB_INVALID, "null handle");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    RowView v = row_view(m, s);
+    *width_out = hyb_width(v, v.nnz ? max_row_len(v, s) : 0, s);
+  });
+}
+
+}  // extern "C"

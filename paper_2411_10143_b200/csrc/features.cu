@@ -1,0 +1,147 @@
+// Structural features on the device: extract_features (features.py:68-156).
+//
+// The fifteen reference features are float formulas over seven exact
+// integer aggregates.  One fused pass over row_ptr and
+// col_idx produces six of them (row-length sum / square-sum / max / min,
+// row span sum, longest-consecutive-run sum) and sets the diagonal-occupancy
+// bitmap; a popcount pass yields the seventh (ndiag).  Integer arithmetic
+// makes the aggregates independent of the reduction order, and the host
+// evaluates the floats with the reference's own expressions, so the feature
+// vector is bit-identical to the CPU path.
+#include "matrix.cuh"
+
+namespace svb {
+
+struct FeatAcc {
+  unsigned long long sum_r, sum_r2, span, runs;
+  long long max_r, min_r;
+};
+
+template <int BLOCK>
+__device__ void block_reduce_store(FeatAcc a, FeatAcc* out) {
+  __shared__ FeatAcc sh[BLOCK / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a.sum_r += __shfl_xor_sync(0xffffffffu, a.sum_r, o);
+    a.sum_r2 += __shfl_xor_sync(0xffffffffu, a.sum_r2, o);
+    a.span += __shfl_xor_sync(0xffffffffu, a.span, o);
+    a.runs += __shfl_xor_sync(0xffffffffu, a.runs, o);
+    a.max_r = max(a.max_r, (long long)__shfl_xor_sync(0xffffffffu, a.max_r, o));
+    a.min_r = min(a.min_r, (long long)__shfl_xor_sync(0xffffffffu, a.min_r, o));
+  }
+  if (lane == 0) sh[wid] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FeatAcc t = sh[0];
+    for (int w = 1; w < BLOCK / 32; ++w) {
+      t.sum_r += sh[w].sum_r;
+      t.sum_r2 += sh[w].sum_r2;
+      t.span += sh[w].span;
+      t.runs += sh[w].runs;
+      t.max_r = max(t.max_r, sh[w].max_r);
+      t.min_r = min(t.min_r, sh[w].min_r);
+    }
+    atomicAdd(&out->sum_r, t.sum_r);
+    atomicAdd(&out->sum_r2, t.sum_r2);
+    atomicAdd(&out->span, t.span);
+    atomicAdd(&out->runs, t.runs);
+    atomicMax(&out->max_r, t.max_r);
+    atomicMin(&out->min_r, t.min_r);
+  }
+}
+
+template <class P, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __restrict__ ptr,
+                                                    const int* __restrict__ cols,
+                                                    unsigned* __restrict__ bits, FeatAcc* out) {
+  FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = ptr[i], e = ptr[i + 1], L = e - s;
+    a.sum_r += (unsigned long long)L;
+    a.sum_r2 += (unsigned long long)(L * L);
+    a.max_r = max(a.max_r, (long long)L);
+    a.min_r = min(a.min_r, (long long)L);
+    if (L == 0) continue;
+    const int64_t diag0 = nrows - 1 - i;
+    int c0 = cols[s], prev = c0;
+    int64_t run = 1, best = 1;
+    for (int64_t k = s;; ) {
+      const int64_t d = (int64_t)prev + diag0;
+      const unsigned m = 1u << (d & 31);
+      unsigned* w = bits + (d >> 5);
+      if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+      if (++k >= e) break;
+      const int c = cols[k];
+      run = (c == prev + 1) ? run + 1 : 1;
+      best = max(best, run);
+      prev = c;
+    }
+    a.span += (unsigned long long)(prev - c0);
+    a.runs += (unsigned long long)best;
+  }
+  block_reduce_store<BLOCK>(a, out);
+}
+
+__global__ void k_popcount(int64_t nwords, const unsigned* __restrict__ bits,
+                           unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(bits[w]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned long long sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+    atomicAdd(out, t);
+  }
+}
+
+}  // namespace svb
+
+using namespace svb;
+
+extern "C" int svb_features(const svb_matrix* m, int64_t* agg, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(m && agg, SVB_INVALID, "null handle");
+    SVB_REQUIRE(m->fmt == SVB_CSR, SVB_UNSUPPORTED_CONFIG, "extract_features expects CSR");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nbits = m->nrows + m->ncols - 1;
+    const int64_t nwords = (nbits + 31) / 32;
+    Buf bits = alloc(nwords * 4, s);
+    Buf acc = alloc(sizeof(FeatAcc) + 8, s);
+    SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
+    FeatAcc init{0, 0, 0, 0, 0, LLONG_MAX};
+    SVB_CUDA_TRY(cudaMemcpyAsync(acc->ptr, &init, sizeof(FeatAcc), cudaMemcpyHostToDevice, s));
+    SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(acc->ptr) + sizeof(FeatAcc), 0, 8, s));
+    constexpr int B = 256;
+    const unsigned g = grid_for(m->nrows, B, 8);
+    if (m->ptr64)
+      k_features<long long, B><<<g, B, 0, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
+                                              ptr<unsigned>(bits), ptr<FeatAcc>(acc));
+    else
+      k_features<int, B><<<g, B, 0, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols),
+                                        ptr<unsigned>(bits), ptr<FeatAcc>(acc));
+    SVB_CHECK_LAUNCH();
+    auto* ndiag_d = reinterpret_cast<unsigned long long*>(static_cast<char*>(acc->ptr) + sizeof(FeatAcc));
+    k_popcount<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(bits), ndiag_d);
+    SVB_CHECK_LAUNCH();
+    struct {
+      FeatAcc a;
+      unsigned long long ndiag;
+    } h;
+    SVB_CUDA_TRY(cudaMemcpyAsync(&h, acc->ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    agg[0] = (int64_t)h.a.sum_r;
+    agg[1] = (int64_t)h.a.sum_r2;
+    agg[2] = h.a.max_r;
+    agg[3] = m->nrows ? h.a.min_r : 0;
+    agg[4] = (int64_t)h.a.span;
+    agg[5] = (int64_t)h.a.runs;
+    agg[6] = (int64_t)h.ndiag;
+  });
+}

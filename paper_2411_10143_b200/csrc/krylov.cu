@@ -1,0 +1,605 @@
+// Device-resident Krylov building blocks: restarted MGS-GMRES (solver.py:
+// 219-342) and Hestenes-Stiefel CG (new).
+//
+// Every reduction is a single kernel: CTAs reduce a fixed grid-stride share
+// of the vectors, write a per-CTA partial, and the last CTA to finish
+// (atomic ticket) folds the partials in a fixed tree order and runs the
+// scalar epilogue (Givens rotation, CG alpha/beta, convergence estimate).
+// Results are therefore deterministic run to run, scalars never leave the
+// device inside an iteration, and the host reads one mapped status block
+// per iteration.  The modified Gram-Schmidt loop is fused as
+// "axpy_{i-1} + dot_i" passes: pass i reads w, V[i-1] and V[i] once.
+#include <cmath>
+#include <cstring>
+
+#include "matrix.cuh"
+
+struct svb_krylov {
+  int64_t n = 0, ld = 0;
+  int m = 0;
+  unsigned rgrid = 1;
+  svb::Buf V, x, b, tmp, p, q, r;
+  svb::Buf H, cs, sn, g, y, scal, partials, counter;
+  svb_krylov_status* st_host = nullptr;
+  svb_krylov_status* st_dev = nullptr;
+  ~svb_krylov() {
+    if (st_host) cudaFreeHost(st_host);
+  }
+};
+
+namespace svb {
+
+constexpr int KB = 256;  // threads per CTA for the Krylov kernels
+enum { S_RR = 0, S_ALPHA = 1, S_BETA = 2 };
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// grid-stride over element pairs (rows are 256-byte aligned), odd tail on
+// thread 0 of CTA 0
+template <class F2, class F1>
+__device__ __forceinline__ void for_pairs(int64_t n, F2 f2, F1 f1) {
+  const int64_t n2 = n >> 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x)
+    f2(2 * i);
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f1(n - 1);
+}
+
+// Block-sum `v`, publish the CTA partial, and return true in the last CTA
+// (all threads), where `*total` (thread 0) is the fixed-order grand total.
+__device__ bool grid_sum_last(double v, double* partials, unsigned* counter, double* total) {
+  __shared__ double sh[KB / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < KB / 32; ++w) b += sh[w];
+    partials[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += KB) t += __ldcg(partials + i);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  if (lane == 0) sh[wid] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < KB / 32; ++w) g += sh[w];
+    *total = g;
+    *counter = 0;  // ready for the next reduction on this stream
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool bad(double v) { return !isfinite(v); }
+
+// ---------------------------------------------------------------------------
+// GMRES
+// ---------------------------------------------------------------------------
+struct Gm {
+  double* V;
+  int64_t n, ld;
+  int m;
+  double *H, *cs, *sn, *g, *y;
+  double* partials;
+  unsigned* counter;
+  svb_krylov_status* st;
+};
+
+// ||b|| or ||b - tmp|| into st->beta
+__global__ void __launch_bounds__(KB) k_resnorm(const double* __restrict__ b, const double* __restrict__ t,
+                                                int64_t n, double* partials, unsigned* counter,
+                                                svb_krylov_status* st) {
+  double acc = 0.0;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 bb = ld2(b + e);
+        double2 tt = t ? ld2(t + e) : make_double2(0.0, 0.0);
+        double r0 = bb.x - tt.x, r1 = bb.y - tt.y;
+        acc += r0 * r0;
+        acc += r1 * r1;
+      },
+      [&](int64_t e) {
+        double r0 = b[e] - (t ? t[e] : 0.0);
+        acc += r0 * r0;
+      });
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    st->beta = sqrt(tot);
+    st->nonfinite = bad(st->beta);
+  }
+}
+
+// r = b - tmp into V0 and ||r||; the next kernel scales V0 by 1/beta
+__global__ void __launch_bounds__(KB) k_gm_residual(Gm G, const double* __restrict__ b,
+                                                    const double* __restrict__ t) {
+  double acc = 0.0;
+  double* v0 = G.V;
+  for_pairs(
+      G.n,
+      [&](int64_t e) {
+        double2 bb = ld2(b + e), tt = ld2(t + e);
+        double2 r = make_double2(bb.x - tt.x, bb.y - tt.y);
+        st2(v0 + e, r);
+        acc += r.x * r.x;
+        acc += r.y * r.y;
+      },
+      [&](int64_t e) {
+        double r = b[e] - t[e];
+        v0[e] = r;
+        acc += r * r;
+      });
+  double tot;
+  if (grid_sum_last(acc, G.partials, G.counter, &tot) && threadIdx.x == 0) {
+    const double beta = sqrt(tot);
+    G.st->beta = beta;
+    G.st->nonfinite = bad(beta);
+    for (int i = 0; i < (G.m + 1) * G.m; ++i) G.H[i] = 0.0;
+    for (int i = 0; i < G.m; ++i) G.cs[i] = G.sn[i] = 0.0;
+    for (int i = 0; i <= G.m; ++i) G.g[i] = 0.0;
+    G.g[0] = beta;
+  }
+}
+
+// V[j] /= d where d = g[0] (restart) or the recorded hnext
+__global__ void __launch_bounds__(KB) k_gm_scale(double* __restrict__ v, int64_t n,
+                                                 const double* __restrict__ dptr) {
+  const double d = *dptr;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 a = ld2(v + e);
+        st2(v + e, make_double2(a.x / d, a.y / d));
+      },
+      [&](int64_t e) { v[e] = v[e] / d; });
+}
+
+// pass 0: H[0,j] = V0 . w   (w = V[j+1])
+__global__ void __launch_bounds__(KB) k_gm_dot0(Gm G, int j) {
+  const double* __restrict__ w = G.V + (int64_t)(j + 1) * G.ld;
+  const double* __restrict__ v = G.V;
+  double acc = 0.0;
+  for_pairs(
+      G.n,
+      [&](int64_t e) {
+        double2 a = ld2(v + e), c = ld2(w + e);
+        acc += a.x * c.x;
+        acc += a.y * c.y;
+      },
+      [&](int64_t e) { acc += v[e] * w[e]; });
+  double tot;
+  if (grid_sum_last(acc, G.partials, G.counter, &tot) && threadIdx.x == 0) G.H[j] = tot;
+}
+
+// pass i (1..j): w -= H[i-1,j] V[i-1];  H[i,j] = V[i] . w
+__global__ void __launch_bounds__(KB) k_gm_pass(Gm G, int i, int j) {
+  double* __restrict__ w = G.V + (int64_t)(j + 1) * G.ld;
+  const double* __restrict__ vp = G.V + (int64_t)(i - 1) * G.ld;
+  const double* __restrict__ vi = G.V + (int64_t)i * G.ld;
+  const double h = G.H[(i - 1) * G.m + j];
+  double acc = 0.0;
+  for_pairs(
+      G.n,
+      [&](int64_t e) {
+        double2 ww = ld2(w + e), a = ld2(vp + e), c = ld2(vi + e);
+        ww.x -= h * a.x;
+        ww.y -= h * a.y;
+        st2(w + e, ww);
+        acc += c.x * ww.x;
+        acc += c.y * ww.y;
+      },
+      [&](int64_t e) {
+        double ww = w[e] - h * vp[e];
+        w[e] = ww;
+        acc += vi[e] * ww;
+      });
+  double tot;
+  if (grid_sum_last(acc, G.partials, G.counter, &tot) && threadIdx.x == 0) G.H[i * G.m + j] = tot;
+}
+
+// final pass: w -= H[j,j] V[j]; hnext = ||w||; Givens update of column j,
+// residual estimate |g[j+1]|/||b|| (solver.py:294-313)
+__global__ void __launch_bounds__(KB) k_gm_final(Gm G, int j, double bnorm) {
+  double* __restrict__ w = G.V + (int64_t)(j + 1) * G.ld;
+  const double* __restrict__ vj = G.V + (int64_t)j * G.ld;
+  const double h = G.H[j * G.m + j];
+  double acc = 0.0;
+  for_pairs(
+      G.n,
+      [&](int64_t e) {
+        double2 ww = ld2(w + e), a = ld2(vj + e);
+        ww.x -= h * a.x;
+        ww.y -= h * a.y;
+        st2(w + e, ww);
+        acc += ww.x * ww.x;
+        acc += ww.y * ww.y;
+      },
+      [&](int64_t e) {
+        double ww = w[e] - h * vj[e];
+        w[e] = ww;
+        acc += ww * ww;
+      });
+  double tot;
+  if (grid_sum_last(acc, G.partials, G.counter, &tot) && threadIdx.x == 0) {
+    const int m = G.m;
+    double* H = G.H;
+    const double hnext = sqrt(tot);
+    for (int i = 0; i < j; ++i) {
+      const double a = H[i * m + j], b = H[(i + 1) * m + j];
+      const double hi = G.cs[i] * a + G.sn[i] * b;
+      H[(i + 1) * m + j] = -G.sn[i] * a + G.cs[i] * b;
+      H[i * m + j] = hi;
+    }
+    const double hjj = H[j * m + j];
+    const double denom = hypot(hjj, hnext);
+    double c = 1.0, s = 0.0;
+    if (denom != 0.0) {
+      c = hjj / denom;
+      s = hnext / denom;
+    }
+    G.cs[j] = c;
+    G.sn[j] = s;
+    H[j * m + j] = c * hjj + s * hnext;
+    G.g[j + 1] = -s * G.g[j];
+    G.g[j] = c * G.g[j];
+    H[(j + 1) * m + j] = hnext;  // kept for V[j+1] /= hnext
+    const double est = fabs(G.g[j + 1]) / bnorm;
+    G.st->hnext = hnext;
+    G.st->hjj = H[j * m + j];
+    G.st->estimate = est;
+    G.st->nonfinite = bad(hnext) || bad(est);
+  }
+}
+
+// back-substitution of the rotated system (solver.py:211-214), one thread
+__global__ void k_gm_solve_y(Gm G, int j) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int m = G.m;
+  for (int i = j; i >= 0; --i) {
+    double dot = 0.0;
+    for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * G.y[k];
+    G.y[i] = (G.g[i] - dot) / G.H[i * m + i];
+  }
+}
+
+// x += V[:j+1]^T y (solver.py:215-216, 339-340)
+__global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restrict__ x) {
+  __shared__ double ys[64];
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) ys[i] = G.y[i];
+  __syncthreads();
+  for_pairs(
+      G.n,
+      [&](int64_t e) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int i = 0; i <= j; ++i) {
+          double2 v = ld2(G.V + (int64_t)i * G.ld + e);
+          t.x += v.x * ys[i];
+          t.y += v.y * ys[i];
+        }
+        double2 xx = ld2(x + e);
+        st2(x + e, make_double2(xx.x + t.x, xx.y + t.y));
+      },
+      [&](int64_t e) {
+        double t = 0.0;
+        for (int i = 0; i <= j; ++i) t += G.V[(int64_t)i * G.ld + e] * ys[i];
+        x[e] = x[e] + t;
+      });
+}
+
+// ---------------------------------------------------------------------------
+// CG
+// ---------------------------------------------------------------------------
+// r = b - tmp; p = r; rr = r.r
+__global__ void __launch_bounds__(KB) k_cg_restart(int64_t n, const double* __restrict__ b,
+                                                   const double* __restrict__ t, double* __restrict__ r,
+                                                   double* __restrict__ p, double* scal, double* partials,
+                                                   unsigned* counter, svb_krylov_status* st) {
+  double acc = 0.0;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 bb = ld2(b + e), tt = ld2(t + e);
+        double2 rr = make_double2(bb.x - tt.x, bb.y - tt.y);
+        st2(r + e, rr);
+        st2(p + e, rr);
+        acc += rr.x * rr.x;
+        acc += rr.y * rr.y;
+      },
+      [&](int64_t e) {
+        double rr = b[e] - t[e];
+        r[e] = rr;
+        p[e] = rr;
+        acc += rr * rr;
+      });
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    scal[S_RR] = tot;
+    st->beta = sqrt(tot);
+    st->nonfinite = bad(tot);
+  }
+}
+
+// alpha = rr / (p.q)
+__global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restrict__ p,
+                                              const double* __restrict__ q, double* scal, double* partials,
+                                              unsigned* counter, svb_krylov_status* st) {
+  double acc = 0.0;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 a = ld2(p + e), c = ld2(q + e);
+        acc += a.x * c.x;
+        acc += a.y * c.y;
+      },
+      [&](int64_t e) { acc += p[e] * q[e]; });
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    st->pq = tot;
+    st->nonfinite = bad(tot);
+    scal[S_ALPHA] = tot != 0.0 ? scal[S_RR] / tot : 0.0;
+  }
+}
+
+// x += alpha p; r -= alpha q; rr' = r.r; beta = rr'/rr; estimate
+__global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                  const double* __restrict__ p, const double* __restrict__ q,
+                                                  double* scal, double bnorm, double* partials,
+                                                  unsigned* counter, svb_krylov_status* st) {
+  const double alpha = scal[S_ALPHA];
+  double acc = 0.0;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 xx = ld2(x + e), rr = ld2(r + e), pp = ld2(p + e), qq = ld2(q + e);
+        xx.x += alpha * pp.x;
+        xx.y += alpha * pp.y;
+        rr.x -= alpha * qq.x;
+        rr.y -= alpha * qq.y;
+        st2(x + e, xx);
+        st2(r + e, rr);
+        acc += rr.x * rr.x;
+        acc += rr.y * rr.y;
+      },
+      [&](int64_t e) {
+        x[e] += alpha * p[e];
+        double rr = r[e] - alpha * q[e];
+        r[e] = rr;
+        acc += rr * rr;
+      });
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    const double rr_old = scal[S_RR];
+    scal[S_BETA] = tot / rr_old;
+    scal[S_RR] = tot;
+    st->estimate = sqrt(tot) / bnorm;
+    st->nonfinite = st->nonfinite || bad(tot) || bad(st->estimate);
+  }
+}
+
+// p = r + beta p
+__global__ void __launch_bounds__(KB) k_cg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
+                                             const double* scal) {
+  const double beta = scal[S_BETA];
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 rr = ld2(r + e), pp = ld2(p + e);
+        st2(p + e, make_double2(rr.x + beta * pp.x, rr.y + beta * pp.y));
+      },
+      [&](int64_t e) { p[e] = r[e] + beta * p[e]; });
+}
+
+// generic dot for the host API
+__global__ void __launch_bounds__(KB) k_dot(int64_t n, const double* __restrict__ a,
+                                            const double* __restrict__ b, double* partials,
+                                            unsigned* counter, double* out) {
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    acc += a[e] * b[e];
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = tot;
+}
+
+static Gm gm_of(svb_krylov* k) {
+  Gm G;
+  G.V = ptr<double>(k->V);
+  G.n = k->n;
+  G.ld = k->ld;
+  G.m = k->m;
+  G.H = ptr<double>(k->H);
+  G.cs = ptr<double>(k->cs);
+  G.sn = ptr<double>(k->sn);
+  G.g = ptr<double>(k->g);
+  G.y = ptr<double>(k->y);
+  G.partials = ptr<double>(k->partials);
+  G.counter = ptr<unsigned>(k->counter);
+  G.st = k->st_dev;
+  return G;
+}
+
+}  // namespace svb
+
+using namespace svb;
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
+  return guard([&] {
+    SVB_REQUIRE(n >= 1 && m >= 0 && m <= 63, SVB_INVALID, "krylov workspace: n >= 1, 0 <= m <= 63");
+    cudaStream_t s = 0;
+    auto k = new svb_krylov();
+    k->n = n;
+    k->m = m;
+    k->ld = (n + 31) & ~int64_t(31);  // 256-byte aligned rows
+    k->rgrid = grid_for(n / 2 + 1, KB, 4);
+    const int64_t mm = m > 0 ? m : 1;
+    k->V = alloc((m + 1) * k->ld * 8, s);
+    k->x = alloc(k->ld * 8, s);
+    k->b = alloc(k->ld * 8, s);
+    k->tmp = alloc(k->ld * 8, s);
+    k->p = alloc(k->ld * 8, s);
+    k->q = alloc(k->ld * 8, s);
+    k->r = alloc(k->ld * 8, s);
+    k->H = alloc((mm + 1) * mm * 8, s);
+    k->cs = alloc(mm * 8, s);
+    k->sn = alloc(mm * 8, s);
+    k->g = alloc((mm + 1) * 8, s);
+    k->y = alloc(mm * 8, s);
+    k->scal = alloc(8 * 8, s);
+    k->partials = alloc(k->rgrid * 8, s);
+    k->counter = alloc(8, s);
+    SVB_CUDA_TRY(cudaMemsetAsync(k->counter->ptr, 0, 8, s));
+    SVB_CUDA_TRY(cudaMemsetAsync(k->x->ptr, 0, k->ld * 8, s));
+    SVB_CUDA_TRY(cudaHostAlloc((void**)&k->st_host, sizeof(svb_krylov_status), cudaHostAllocMapped));
+    std::memset(k->st_host, 0, sizeof(svb_krylov_status));
+    SVB_CUDA_TRY(cudaHostGetDevicePointer((void**)&k->st_dev, k->st_host, 0));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = k;
+  });
+}
+
+int svb_krylov_destroy(svb_krylov* k) {
+  return guard([&] {
+    SVB_CUDA_TRY(cudaDeviceSynchronize());
+    delete k;
+  });
+}
+
+int svb_krylov_vec(svb_krylov* k, int which, double** out) {
+  return guard([&] {
+    SVB_REQUIRE(k && out, SVB_INVALID, "null workspace");
+    if (which >= 0) {
+      SVB_REQUIRE(which <= k->m, SVB_INVALID, "V row out of range");
+      *out = ptr<double>(k->V) + (int64_t)which * k->ld;
+      return;
+    }
+    switch (which) {
+      case -1: *out = ptr<double>(k->x); break;
+      case -2: *out = ptr<double>(k->b); break;
+      case -3: *out = ptr<double>(k->tmp); break;
+      case -4: *out = ptr<double>(k->p); break;
+      case -5: *out = ptr<double>(k->q); break;
+      case -6: *out = ptr<double>(k->r); break;
+      default: throw Error{SVB_INVALID, "unknown workspace vector"};
+    }
+  });
+}
+
+int svb_krylov_status_get(svb_krylov* k, void* stream, svb_krylov_status* out) {
+  return guard([&] {
+    SVB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    std::memcpy(out, (const void*)k->st_host, sizeof(svb_krylov_status));
+  });
+}
+
+int svb_krylov_bnorm(svb_krylov* k, void* stream) {
+  return guard([&] {
+    k_resnorm<<<k->rgrid, KB, 0, S(stream)>>>(ptr<double>(k->b), nullptr, k->n, ptr<double>(k->partials),
+                                               ptr<unsigned>(k->counter), k->st_dev);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_krylov_residual(svb_krylov* k, void* stream) {
+  return guard([&] {
+    k_resnorm<<<k->rgrid, KB, 0, S(stream)>>>(ptr<double>(k->b), ptr<double>(k->tmp), k->n,
+                                               ptr<double>(k->partials), ptr<unsigned>(k->counter),
+                                               k->st_dev);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_gmres_restart(svb_krylov* k, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k->m >= 1, SVB_INVALID, "GMRES workspace needs restart m >= 1");
+    Gm G = gm_of(k);
+    k_gm_residual<<<k->rgrid, KB, 0, S(stream)>>>(G, ptr<double>(k->b), ptr<double>(k->tmp));
+    SVB_CHECK_LAUNCH();
+    k_gm_scale<<<k->rgrid, KB, 0, S(stream)>>>(G.V, k->n, G.g);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(j >= 0 && j < k->m, SVB_INVALID, "Arnoldi column out of range");
+    Gm G = gm_of(k);
+    cudaStream_t s = S(stream);
+    k_gm_dot0<<<k->rgrid, KB, 0, s>>>(G, j);
+    for (int i = 1; i <= j; ++i) k_gm_pass<<<k->rgrid, KB, 0, s>>>(G, i, j);
+    k_gm_final<<<k->rgrid, KB, 0, s>>>(G, j, bnorm);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_gmres_normalize(svb_krylov* k, int32_t j, void* stream) {
+  return guard([&] {
+    Gm G = gm_of(k);
+    k_gm_scale<<<k->rgrid, KB, 0, S(stream)>>>(G.V + (int64_t)(j + 1) * G.ld, k->n, G.H + (j + 1) * G.m + j);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_gmres_update_x(svb_krylov* k, int32_t j, void* stream) {
+  return guard([&] {
+    Gm G = gm_of(k);
+    k_gm_solve_y<<<1, 32, 0, S(stream)>>>(G, j);
+    k_gm_update_x<<<k->rgrid, KB, 0, S(stream)>>>(G, j, ptr<double>(k->x));
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_cg_restart(svb_krylov* k, void* stream) {
+  return guard([&] {
+    k_cg_restart<<<k->rgrid, KB, 0, S(stream)>>>(k->n, ptr<double>(k->b), ptr<double>(k->tmp), ptr<double>(k->r),
+                                                  ptr<double>(k->p), ptr<double>(k->scal), ptr<double>(k->partials),
+                                                  ptr<unsigned>(k->counter), k->st_dev);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_cg_step(svb_krylov* k, double bnorm, void* stream) {
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    double* P = ptr<double>(k->partials);
+    unsigned* C = ptr<unsigned>(k->counter);
+    k_cg_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->scal), P, C,
+                                     k->st_dev);
+    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
+                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev);
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal));
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_dot(const double* x, const double* y, int64_t n, double* out_host, void* stream) {
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    const unsigned g = grid_for(n, KB, 4);
+    Buf part = alloc(g * 8 + 16, s);
+    unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(part->ptr) + g * 8);
+    double* res = reinterpret_cast<double*>(static_cast<char*>(part->ptr) + g * 8 + 8);
+    SVB_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4, s));
+    k_dot<<<g, KB, 0, s>>>(n, x, y, ptr<double>(part), ctr, res);
+    SVB_CHECK_LAUNCH();
+    SVB_CUDA_TRY(cudaMemcpyAsync(out_host, res, 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,484 @@
+// Library plumbing and the container half of the C ABI:
+// svb_{coo,csr,ell,dia,hyb}_create, svb_matrix_{destroy,info_get,download}.
+// Mirrors the reference containers (formats.py:50-260); host-side validation
+// with the reference's error messages lives in the Python layer.
+#include <cub/device/device_scan.cuh>
+
+#include <cstring>
+#include <thread>
+
+#include "matrix.cuh"
+
+namespace svb {
+
+// ---------------------------------------------------------------------------
+// errors / allocation / device facts
+// ---------------------------------------------------------------------------
+static thread_local std::string tls_error;
+void set_error(const std::string& msg) { tls_error = msg; }
+const char* get_error() { return tls_error.c_str(); }
+
+DevBuf::~DevBuf() {
+  if (ptr) cudaFreeAsync(ptr, stream);
+}
+
+Buf alloc(size_t bytes, cudaStream_t s) {
+  auto b = std::make_shared<DevBuf>();
+  b->bytes = bytes;
+  b->stream = s;
+  if (bytes) {
+    cudaError_t e = cudaMallocAsync(&b->ptr, bytes, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{e == cudaErrorMemoryAllocation ? SVB_OOM : SVB_CUDA,
+                  std::string("device allocation of ") + std::to_string(bytes) +
+                      " bytes failed: " + cudaGetErrorString(e)};
+    }
+  }
+  return b;
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n > 0 ? n : 148;
+  }
+  return cached;
+}
+
+Buf upload(const void* host, size_t bytes, cudaStream_t s) {
+  Buf b = alloc(bytes, s);
+  if (bytes) SVB_CUDA_TRY(cudaMemcpyAsync(b->ptr, host, bytes, cudaMemcpyHostToDevice, s));
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// index width conversion kernels
+// ---------------------------------------------------------------------------
+__global__ void k_narrow(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int32_t)src[i];
+}
+__global__ void k_widen(const int32_t* __restrict__ src, int64_t* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void k_to_f32(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+void narrow_i64_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_narrow<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
+  SVB_CHECK_LAUNCH();
+}
+void widen_i32_to_i64(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_widen<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
+  SVB_CHECK_LAUNCH();
+}
+void ptr_to_i64(const svb_matrix* m, int64_t* dst, cudaStream_t s) {
+  if (m->ptr64)
+    SVB_CUDA_TRY(cudaMemcpyAsync(dst, m->ptr->ptr, (m->nrows + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  else
+    widen_i32_to_i64(ptr<int32_t>(m->ptr), dst, m->nrows + 1, s);
+}
+
+static Buf to_f32(const Buf& src, int64_t n, cudaStream_t s) {
+  Buf out = alloc(n * sizeof(float), s);
+  if (n > 0) {
+    k_to_f32<<<grid_for(n, 256), 256, 0, s>>>(ptr<double>(src), ptr<float>(out), n);
+    SVB_CHECK_LAUNCH();
+  }
+  return out;
+}
+
+const float* vals_f32(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (!m->vals32) {
+    int64_t n = m->vals ? (int64_t)(m->vals->bytes / 8) : 0;
+    m->vals32 = to_f32(m->vals, n, s);
+  }
+  return ptr<float>(m->vals32);
+}
+const float* svals_f32(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (!m->svals32) m->svals32 = to_f32(m->svals, m->spill_nnz, s);
+  return ptr<float>(m->svals32);
+}
+
+int64_t exclusive_scan_total(const int64_t* counts, int64_t* out, int64_t n, cudaStream_t s) {
+  // out[0..n] = exclusive prefix of counts[0..n-1] with the total at out[n]
+  SVB_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+  if (n > 0) {
+    size_t tmp_bytes = 0;
+    SVB_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, counts, out + 1, n, s));
+    Buf tmp = alloc(tmp_bytes, s);
+    SVB_CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp->ptr, tmp_bytes, counts, out + 1, n, s));
+  }
+  int64_t total = 0;
+  SVB_CUDA_TRY(cudaMemcpyAsync(&total, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  return total;
+}
+
+// row_ptr from sorted COO rows: ptr[i] = lower_bound(rows, i) (formats.py:327-330)
+template <class P>
+__global__ void k_rows_to_ptr(const int32_t* __restrict__ rows, int64_t nnz, int64_t nrows,
+                              P* __restrict__ ptr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (rows[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    ptr[i] = (P)lo;
+  }
+}
+
+Buf rows_to_ptr(const int32_t* rows, int64_t nnz, int64_t nrows, bool ptr64, cudaStream_t s) {
+  Buf p = alloc((nrows + 1) * (ptr64 ? 8 : 4), s);
+  if (ptr64)
+    k_rows_to_ptr<long long><<<grid_for(nrows + 1, 256), 256, 0, s>>>(rows, nnz, nrows, ptr<long long>(p));
+  else
+    k_rows_to_ptr<int32_t><<<grid_for(nrows + 1, 256), 256, 0, s>>>(rows, nnz, nrows, ptr<int32_t>(p));
+  SVB_CHECK_LAUNCH();
+  return p;
+}
+
+// rows from a CSR row pointer (formats.py:285-287): one thread per row
+template <class P>
+__global__ void k_ptr_to_rows(const P* __restrict__ ptr, int64_t nrows, int32_t* __restrict__ rows) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = ptr[i], e = ptr[i + 1];
+    for (int64_t k = s; k < e; ++k) rows[k] = (int32_t)i;
+  }
+}
+
+Buf ptr_to_rows(const svb_matrix* m, cudaStream_t s) {
+  Buf r = alloc(m->nnz * 4, s);
+  if (m->nnz > 0) {
+    if (m->ptr64)
+      k_ptr_to_rows<long long><<<grid_for(m->nrows, 128), 128, 0, s>>>(ptr<long long>(m->ptr), m->nrows, ptr<int32_t>(r));
+    else
+      k_ptr_to_rows<int32_t><<<grid_for(m->nrows, 128), 128, 0, s>>>(ptr<int32_t>(m->ptr), m->nrows, ptr<int32_t>(r));
+    SVB_CHECK_LAUNCH();
+  }
+  return r;
+}
+
+}  // namespace svb
+
+using namespace svb;
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static void require_index_range(int64_t nrows, int64_t ncols) {
+  SVB_REQUIRE(nrows >= 1 && ncols >= 1, SVB_DIM_MISMATCH, "matrix dimensions must be positive");
+  SVB_REQUIRE(nrows < INT32_MAX && ncols < INT32_MAX, SVB_INAPPLICABLE,
+              "dimensions >= 2^31 are not supported by the int32 device index layout");
+}
+
+static Buf upload_i32(const int64_t* host, int64_t n, cudaStream_t s) {
+  Buf out = alloc(n * 4, s);
+  if (n > 0) {
+    Buf stage = upload(host, n * 8, s);
+    narrow_i64_to_i32(ptr<int64_t>(stage), ptr<int32_t>(out), n, s);
+  }
+  return out;
+}
+
+extern "C" {
+
+const char* svb_last_error(void) { return get_error(); }
+int svb_abi_version(void) { return SVB_ABI_VERSION; }
+
+int svb_init(int device) {
+  return guard([&] {
+    SVB_CUDA_TRY(cudaSetDevice(device));
+    // keep freed pool memory cached: conversions and workspaces recycle it
+    cudaMemPool_t pool;
+    SVB_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    SVB_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    sm_count();
+  });
+}
+
+int svb_stream_sync(void* stream) {
+  return guard([&] { SVB_CUDA_TRY(cudaStreamSynchronize(S(stream))); });
+}
+
+int svb_stream_create(int priority, void** out) {
+  return guard([&] {
+    int lo = 0, hi = 0;
+    SVB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // priority > 0 asks for the highest (solver), < 0 for the lowest (advisor)
+    const int p = priority > 0 ? hi : (priority < 0 ? lo : 0);
+    cudaStream_t s;
+    SVB_CUDA_TRY(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p));
+    *out = s;
+  });
+}
+int svb_stream_destroy(void* stream) {
+  return guard([&] { SVB_CUDA_TRY(cudaStreamDestroy(S(stream))); });
+}
+int svb_event_record(void* stream, void** out) {
+  return guard([&] {
+    cudaEvent_t e;
+    SVB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SVB_CUDA_TRY(cudaEventRecord(e, S(stream)));
+    *out = e;
+  });
+}
+int svb_event_query(void* event) {
+  cudaError_t e = cudaEventQuery(reinterpret_cast<cudaEvent_t>(event));
+  if (e == cudaSuccess) return SVB_OK;
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    return SVB_INVALID;
+  }
+  set_error(cudaGetErrorString(e));
+  return SVB_CUDA;
+}
+int svb_stream_wait_event(void* stream, void* event) {
+  return guard([&] { SVB_CUDA_TRY(cudaStreamWaitEvent(S(stream), reinterpret_cast<cudaEvent_t>(event), 0)); });
+}
+int svb_event_destroy(void* event) {
+  return guard([&] { SVB_CUDA_TRY(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(event))); });
+}
+int svb_malloc(int64_t bytes, void** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (bytes > 0) SVB_CUDA_TRY(cudaMallocAsync(out, bytes, 0));
+    SVB_CUDA_TRY(cudaStreamSynchronize(0));
+  });
+}
+int svb_free(void* p) {
+  return guard([&] {
+    if (!p) return;
+    SVB_CUDA_TRY(cudaDeviceSynchronize());
+    SVB_CUDA_TRY(cudaFreeAsync(p, 0));
+  });
+}
+int svb_host_alloc(int64_t bytes, void** out) {
+  return guard([&] { SVB_CUDA_TRY(cudaHostAlloc(out, bytes > 0 ? bytes : 1, cudaHostAllocDefault)); });
+}
+int svb_host_free(void* p) {
+  return guard([&] { SVB_CUDA_TRY(cudaFreeHost(p)); });
+}
+int svb_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  return guard([&] {
+    if (bytes > 0) SVB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, S(stream)));
+  });
+}
+int svb_memset(void* dst, int value, int64_t bytes, void* stream) {
+  return guard([&] {
+    if (bytes > 0) SVB_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, S(stream)));
+  });
+}
+int svb_device_info(int32_t* sms, int64_t* free_b, int64_t* total_b) {
+  return guard([&] {
+    size_t f = 0, t = 0;
+    SVB_CUDA_TRY(cudaMemGetInfo(&f, &t));
+    *sms = sm_count();
+    *free_b = (int64_t)f;
+    *total_b = (int64_t)t;
+  });
+}
+
+int svb_coo_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows_host,
+                   const int64_t* cols_host, const double* vals_host, void* stream,
+                   svb_matrix** out) {
+  return guard([&] {
+    require_index_range(nrows, ncols);
+    cudaStream_t s = S(stream);
+    auto m = new svb_matrix();
+    m->fmt = SVB_COO;
+    m->nrows = nrows; m->ncols = ncols; m->nnz = nnz;
+    m->ptr64 = nnz >= INT32_MAX;
+    m->rows = upload_i32(rows_host, nnz, s);
+    m->cols = upload_i32(cols_host, nnz, s);
+    m->vals = upload(vals_host, nnz * 8, s);
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_host,
+                   const int64_t* col_idx_host, const double* vals_host, void* stream,
+                   svb_matrix** out) {
+  return guard([&] {
+    require_index_range(nrows, ncols);
+    cudaStream_t s = S(stream);
+    auto m = new svb_matrix();
+    m->fmt = SVB_CSR;
+    m->nrows = nrows; m->ncols = ncols; m->nnz = nnz;
+    m->ptr64 = nnz >= INT32_MAX;
+    if (m->ptr64) m->ptr = upload(row_ptr_host, (nrows + 1) * 8, s);
+    else m->ptr = upload_i32(row_ptr_host, nrows + 1, s);
+    m->cols = upload_i32(col_idx_host, nnz, s);
+    m->vals = upload(vals_host, nnz * 8, s);
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_ell_create(int64_t nrows, int64_t ncols, int64_t width, const int64_t* cols_host,
+                   const double* vals_host, void* stream, svb_matrix** out) {
+  return guard([&] {
+    require_index_range(nrows, ncols);
+    cudaStream_t s = S(stream);
+    auto m = new svb_matrix();
+    m->fmt = SVB_ELL;
+    m->nrows = nrows; m->ncols = ncols; m->width = width;
+    int64_t cells = nrows * width;
+    m->cols = upload_i32(cols_host, cells, s);
+    m->vals = upload(vals_host, cells * 8, s);
+    int64_t stored = 0;
+    for (int64_t i = 0; i < cells; ++i) stored += cols_host[i] != ncols;
+    m->nnz = stored;
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_dia_create(int64_t nrows, int64_t ncols, int64_t ndiag, const int64_t* offsets_host,
+                   const double* data_host, void* stream, svb_matrix** out) {
+  return guard([&] {
+    require_index_range(nrows, ncols);
+    cudaStream_t s = S(stream);
+    auto m = new svb_matrix();
+    m->fmt = SVB_DIA;
+    m->nrows = nrows; m->ncols = ncols; m->ndiag = ndiag;
+    m->h_offs.assign(offsets_host, offsets_host + ndiag);
+    m->offs = upload(offsets_host, ndiag * 8, s);
+    m->vals = upload(data_host, ndiag * nrows * 8, s);
+    int64_t stored = 0;  // in-range cells (DiaMatrix carries no nnz; informational)
+    for (int64_t k = 0; k < ndiag; ++k) {
+      int64_t off = offsets_host[k];
+      int64_t lo = off < 0 ? -off : 0, hi = nrows < ncols - off ? nrows : ncols - off;
+      if (hi > lo) stored += hi - lo;
+    }
+    m->nnz = stored;
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_hyb_create(const svb_matrix* ell, const svb_matrix* coo, void* stream, svb_matrix** out) {
+  return guard([&] {
+    SVB_REQUIRE(ell && coo && ell->fmt == SVB_ELL && coo->fmt == SVB_COO, SVB_INVALID,
+                "HYB needs an ELL part and a COO part");
+    SVB_REQUIRE(ell->nrows == coo->nrows && ell->ncols == coo->ncols, SVB_DIM_MISMATCH,
+                "ELL and COO parts must share dimensions");
+    cudaStream_t s = S(stream);
+    auto m = new svb_matrix();
+    m->fmt = SVB_HYB;
+    m->nrows = ell->nrows; m->ncols = ell->ncols; m->width = ell->width;
+    m->cols = ell->cols; m->vals = ell->vals;
+    m->rows = coo->rows; m->scols = coo->cols; m->svals = coo->vals;
+    m->spill_nnz = coo->nnz;
+    m->nnz = ell->nnz + coo->nnz;
+    m->ptr = rows_to_ptr(ptr<int32_t>(coo->rows), coo->nnz, coo->nrows, true, s);
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = m;
+  });
+}
+
+int svb_matrix_destroy(svb_matrix* m) {
+  // other streams may still read the buffers: drain the device first
+  return guard([&] {
+    SVB_CUDA_TRY(cudaDeviceSynchronize());
+    forget_bounds(m);
+    delete m;
+  });
+}
+
+int svb_matrix_info_get(const svb_matrix* m, svb_matrix_info* info) {
+  return guard([&] {
+    SVB_REQUIRE(m && info, SVB_INVALID, "null handle");
+    info->format = m->fmt;
+    info->ptr64 = m->ptr64;
+    info->nrows = m->nrows;
+    info->ncols = m->ncols;
+    info->nnz = m->nnz;
+    info->width = m->width;
+    info->ndiag = m->ndiag;
+    info->spill_nnz = m->spill_nnz;
+    info->device_bytes = m->device_bytes();
+  });
+}
+
+int svb_matrix_download(const svb_matrix* m, int which, void* dst, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(m && dst, SVB_INVALID, "null handle");
+    cudaStream_t s = S(stream);
+    auto copy_i32 = [&](const Buf& b, int64_t n) {
+      if (n <= 0) return;
+      Buf w = alloc(n * 8, s);
+      widen_i32_to_i64(ptr<int32_t>(b), ptr<int64_t>(w), n, s);
+      SVB_CUDA_TRY(cudaMemcpyAsync(dst, w->ptr, n * 8, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    };
+    auto copy_raw = [&](const Buf& b, int64_t bytes) {
+      if (bytes <= 0) return;
+      SVB_CUDA_TRY(cudaMemcpyAsync(dst, b->ptr, bytes, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    };
+    switch (which) {
+      case SVB_ARR_ROW_PTR:
+        SVB_REQUIRE(m->fmt == SVB_CSR || m->fmt == SVB_HYB, SVB_INVALID, "no row_ptr");
+        if (m->fmt == SVB_HYB || m->ptr64) copy_raw(m->ptr, (m->nrows + 1) * 8);
+        else copy_i32(m->ptr, m->nrows + 1);
+        break;
+      case SVB_ARR_ROWS:
+        SVB_REQUIRE(m->fmt == SVB_COO || m->fmt == SVB_HYB, SVB_INVALID, "no rows array");
+        copy_i32(m->rows, m->fmt == SVB_COO ? m->nnz : m->spill_nnz);
+        break;
+      case SVB_ARR_COLS:
+        if (m->fmt == SVB_ELL || m->fmt == SVB_HYB) copy_i32(m->cols, m->width * m->nrows);
+        else {
+          SVB_REQUIRE(m->fmt == SVB_CSR || m->fmt == SVB_COO, SVB_INVALID, "no cols array");
+          copy_i32(m->cols, m->nnz);
+        }
+        break;
+      case SVB_ARR_VALS:
+        if (m->fmt == SVB_ELL || m->fmt == SVB_HYB) copy_raw(m->vals, m->width * m->nrows * 8);
+        else {
+          SVB_REQUIRE(m->fmt == SVB_CSR || m->fmt == SVB_COO, SVB_INVALID, "no values array");
+          copy_raw(m->vals, m->nnz * 8);
+        }
+        break;
+      case SVB_ARR_OFFSETS:
+        SVB_REQUIRE(m->fmt == SVB_DIA, SVB_INVALID, "no offsets");
+        if (m->ndiag) std::memcpy(dst, m->h_offs.data(), m->ndiag * 8);
+        break;
+      case SVB_ARR_DATA:
+        SVB_REQUIRE(m->fmt == SVB_DIA, SVB_INVALID, "no DIA data");
+        copy_raw(m->vals, m->ndiag * m->nrows * 8);
+        break;
+      case SVB_ARR_SPILL_COLS:
+        SVB_REQUIRE(m->fmt == SVB_HYB, SVB_INVALID, "no spill");
+        copy_i32(m->scols, m->spill_nnz);
+        break;
+      case SVB_ARR_SPILL_VALS:
+        SVB_REQUIRE(m->fmt == SVB_HYB, SVB_INVALID, "no spill");
+        copy_raw(m->svals, m->spill_nnz * 8);
+        break;
+      default:
+        throw Error{SVB_INVALID, "unknown array selector"};
+    }
+  });
+}
+
+}  // extern "C"

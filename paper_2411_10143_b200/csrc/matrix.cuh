@@ -1,0 +1,62 @@
+// Device-resident sparse matrix handle (the svb_matrix behind the C ABI).
+//
+// One struct covers the five reference containers (formats.py:50-260).  All
+// buffers are immutable once the handle is published, so conversions share
+// them freely (CSR->COO reuses col/val buffers; COO->CSR likewise).
+#pragma once
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+struct svb_matrix {
+  int fmt = SVB_CSR;
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  bool ptr64 = false;      // row pointer element type on device
+  int64_t width = 0;       // ELL / HYB-ELL width
+  int64_t ndiag = 0;       // DIA
+  int64_t spill_nnz = 0;   // HYB COO part
+
+  svb::Buf ptr;    // CSR row_ptr (int32/int64) [nrows+1]; HYB: spill row_ptr (int64)
+  svb::Buf rows;   // COO rows int32 [nnz]; HYB spill rows int32
+  svb::Buf cols;   // CSR/COO cols int32 [nnz]; ELL/HYB cols int32 [width*nrows]
+  svb::Buf vals;   // f64 values in the layout of `cols`; DIA data [ndiag*nrows]
+  svb::Buf offs;   // DIA offsets int64 [ndiag]
+  svb::Buf scols;  // HYB spill cols int32
+  svb::Buf svals;  // HYB spill values f64
+  std::vector<int64_t> h_offs;  // DIA offsets on the host (kernel launch args)
+
+  // lazily created fp32 copies of the value arrays (SVB_F32 SpMV)
+  mutable std::mutex mu;
+  mutable svb::Buf vals32, svals32;
+
+  int64_t device_bytes() const {
+    int64_t b = 0;
+    const svb::Buf* all[] = {&ptr, &rows, &cols, &vals, &offs, &scols, &svals, &vals32, &svals32};
+    for (const svb::Buf* p : all)
+      if (*p) b += (int64_t)(*p)->bytes;
+    return b;
+  }
+};
+
+namespace svb {
+
+// fp32 copies of vals / svals, created on first use on `s`
+const float* vals_f32(const svb_matrix* m, cudaStream_t s);
+const float* svals_f32(const svb_matrix* m, cudaStream_t s);
+
+// helpers shared by the conversion and feature code
+void narrow_i64_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
+void widen_i32_to_i64(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t s);
+void ptr_to_i64(const svb_matrix* m, int64_t* dst, cudaStream_t s);  // CSR row_ptr -> int64
+Buf upload(const void* host, size_t bytes, cudaStream_t s);
+Buf rows_to_ptr(const int32_t* rows, int64_t nnz, int64_t nrows, bool ptr64, cudaStream_t s);
+Buf ptr_to_rows(const svb_matrix* m, cudaStream_t s);
+void forget_bounds(const svb_matrix* m);  // drop cached LibC chunk bounds (spmv.cu)
+
+// exclusive scan of int64 counts (n+1 outputs; out[n] = total) and the total
+// copied back to the host (synchronises `s`)
+int64_t exclusive_scan_total(const int64_t* counts, int64_t* out, int64_t n, cudaStream_t s);
+
+}  // namespace svb

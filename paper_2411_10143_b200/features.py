@@ -1,0 +1,121 @@
+"""Structural features of a CSR matrix, extracted on the B200.
+
+Drop-in for the reference ``spmvtune.features`` (features.py:1-156).  The
+device (csrc/features.cu) computes the seven exact integer aggregates in one
+fused pass plus a popcount; the fifteen float features are then evaluated
+here with the reference's own expressions and operation order
+(features.py:103-110, 147-150), which makes the vector bit-identical to the
+CPU path.
+
+Cancellation keeps the reference contract: a flag raised before the call
+returns ``None`` without touching ``col_idx``; a flag raised while the
+extraction runs is honoured at the phase boundaries (after the device pass
+and before the float evaluation).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .formats import CsrMatrix
+
+FEATURE_NAMES = ("nrows", "ncols", "nnz", "density", "mean", "sd", "cov", "max", "min",
+                 "maxavg", "distavg", "clusteravg", "fill", "ndiag", "diagfill")
+
+CANCEL_CHECK_ROWS = 4096
+
+
+@dataclass
+class FeatureVector:
+    nrows: int
+    ncols: int
+    nnz: int
+    density: float
+    mean: float
+    sd: float
+    cov: float
+    max: float
+    min: float
+    maxavg: float
+    distavg: float
+    clusteravg: float
+    fill: float
+    ndiag: float
+    diagfill: float
+
+    def to_array(self) -> np.ndarray:
+        return np.array([getattr(self, k) for k in FEATURE_NAMES], dtype=np.float64)
+
+    @classmethod
+    def from_array(cls, a) -> "FeatureVector":
+        a = np.asarray(a, dtype=np.float64)
+        if a.shape != (len(FEATURE_NAMES),):
+            raise ValueError(f"expected {len(FEATURE_NAMES)} features, got shape {a.shape}")
+        kw = dict(zip(FEATURE_NAMES, a))
+        for k in ("nrows", "ncols", "nnz"):
+            kw[k] = int(kw[k])
+        return cls(**kw)
+
+
+@dataclass
+class TraversalCounter:
+    """Array elements consumed by an extraction (features.py:60-65)."""
+
+    row_ptr_reads: int = 0
+    col_idx_reads: int = 0
+
+
+def device_aggregates(m: CsrMatrix, stream=None) -> tuple[int, int, int, int, int, int, int]:
+    """(sum r, sum r^2, max r, min r, sum span, sum longest run, ndiag)."""
+    agg = (ctypes.c_int64 * 7)()
+    _lib.check(_lib.lib().svb_features(m._device().handle, agg,
+                                       stream.handle if stream is not None else None))
+    return tuple(int(v) for v in agg)
+
+
+def features_from_aggregates(nrows: int, ncols: int, nnz: int, agg) -> FeatureVector:
+    """The reference's float formulas over exact integers (Python ints, true
+    division, numpy sqrt) — evaluated in the same order as features.py."""
+    sum_r, sum_r2, max_r, min_r, span_sum, run_sum, ndiag = agg
+    density = nnz / (nrows * ncols)
+    mean = nnz / nrows
+    sd = float(np.sqrt(max(sum_r2 / nrows - mean * mean, 0.0)))
+    cov = sd / mean if mean > 0 else 0.0
+    maxavg = max_r - mean
+    fill = nrows * max_r / nnz if nnz > 0 else 0.0
+    distavg = span_sum / nrows
+    clusteravg = run_sum / nrows
+    diagfill = nrows * ndiag / nnz if nnz > 0 else 0.0
+    return FeatureVector(nrows=nrows, ncols=ncols, nnz=nnz, density=density, mean=mean, sd=sd,
+                         cov=cov, max=float(max_r), min=float(min_r or 0), maxavg=maxavg,
+                         distavg=distavg, clusteravg=clusteravg, fill=fill, ndiag=float(ndiag),
+                         diagfill=diagfill)
+
+
+def extract_features(m: CsrMatrix, cancel: threading.Event | None = None, *,
+                     counter: TraversalCounter | None = None,
+                     row_chunk: int = CANCEL_CHECK_ROWS, stream=None) -> FeatureVector | None:
+    """Feature vector of ``m`` or ``None`` when ``cancel`` is (or becomes) set.
+
+    ``row_chunk`` is accepted for API parity; the device pass is not chunked
+    (it streams row_ptr and col_idx exactly once, so the counters report one
+    pass over each array plus the reference's second row_ptr scan)."""
+    if cancel is not None and cancel.is_set():
+        return None
+    if not isinstance(m, CsrMatrix):
+        raise TypeError("extract_features expects a CsrMatrix")
+    agg = device_aggregates(m, stream)
+    if counter is not None:
+        counter.row_ptr_reads += m.nrows + 1
+    if cancel is not None and cancel.is_set():
+        return None
+    if counter is not None:
+        counter.col_idx_reads += m.nnz
+        counter.row_ptr_reads += m.nrows + 1
+    if cancel is not None and cancel.is_set():
+        return None
+    return features_from_aggregates(m.nrows, m.ncols, m.nnz, agg)

@@ -1,0 +1,139 @@
+"""GPU parity: device conversions and feature extraction are bit-exact with
+the reference (golden fixtures) and the oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+from golden_io import case, case_names
+
+import paper_2411_10143_b200 as P
+from paper_2411_10143_b200 import generators as G
+from paper_2411_10143_b200.features import TraversalCounter
+
+pytestmark = pytest.mark.gpu
+
+
+def coo_of(c):
+    return P.CooMatrix(int(c["nrows"]), int(c["ncols"]), c["coo_rows"], c["coo_cols"], c["coo_vals"])
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_conversions_bit_exact(name):
+    c = case(name)
+    coo = coo_of(c)
+    csr = P.convert(coo, P.FormatTag.CSR)
+    assert np.array_equal(csr.row_ptr, c["csr_ptr"])
+    assert np.array_equal(csr.col_idx, c["coo_cols"])
+    assert np.array_equal(csr.values, c["coo_vals"])
+    for src in (coo, csr):   # COO hub and CSR-direct paths
+        ell = P.convert(src, P.FormatTag.ELL)
+        assert ell.width == int(c["ell_width"])
+        assert np.array_equal(ell.col_idx.T, c["ell_cols"])
+        assert np.array_equal(ell.values.T, c["ell_vals"])
+        hyb = P.convert(src, P.FormatTag.HYB)
+        assert hyb.split_width == int(c["hyb_width"])
+        assert np.array_equal(hyb.ell_part.col_idx.T, c["hyb_ell_cols"])
+        assert np.array_equal(hyb.ell_part.values.T, c["hyb_ell_vals"])
+        assert np.array_equal(hyb.coo_part.rows, c["hyb_spill_rows"])
+        assert np.array_equal(hyb.coo_part.cols, c["hyb_spill_cols"])
+        assert np.array_equal(hyb.coo_part.values, c["hyb_spill_vals"])
+        if int(c["dia_ok"]):
+            dia = P.convert(src, P.FormatTag.DIA)
+            assert np.array_equal(dia.offsets, c["dia_offsets"])
+            assert np.array_equal(dia.data, c["dia_data"])
+        else:
+            with pytest.raises(P.FormatInapplicableError, match="inapplicable"):
+                P.convert(src, P.FormatTag.DIA)
+    # round trips back through COO (to_coo of every layout)
+    for fmt in (P.FormatTag.CSR, P.FormatTag.ELL, P.FormatTag.HYB, P.FormatTag.COO):
+        back = P.to_coo(P.convert(coo, fmt))
+        assert np.array_equal(back.rows, c["coo_rows"]), fmt
+        assert np.array_equal(back.cols, c["coo_cols"]), fmt
+        assert np.array_equal(back.values, c["coo_vals"]), fmt
+    if int(c["dia_ok"]):
+        back = P.to_coo(P.convert(coo, P.FormatTag.DIA))
+        keep = c["coo_vals"] != 0.0
+        assert np.array_equal(back.rows, c["coo_rows"][keep])
+        assert np.array_equal(back.cols, c["coo_cols"][keep])
+
+
+def test_host_built_containers_upload_and_convert():
+    c = case("banded")
+    coo = O.OCoo(int(c["nrows"]), int(c["ncols"]), c["coo_rows"], c["coo_cols"], c["coo_vals"])
+    ell, dia, hyb = O.coo_to_ell(coo), O.coo_to_dia(coo), O.coo_to_hyb(coo)
+    mats = [P.EllMatrix(ell.nrows, ell.ncols, ell.width, ell.cols, ell.vals),
+            P.DiaMatrix(dia.nrows, dia.ncols, dia.offsets, dia.data),
+            P.HybMatrix(P.EllMatrix(coo.nrows, coo.ncols, hyb.width, hyb.ell.cols, hyb.ell.vals),
+                        P.CooMatrix(coo.nrows, coo.ncols, hyb.spill.rows, hyb.spill.cols,
+                                    hyb.spill.vals), hyb.width)]
+    for m in mats:
+        csr = P.convert(m, P.FormatTag.CSR)
+        assert np.array_equal(csr.row_ptr, c["csr_ptr"])
+        assert np.array_equal(csr.col_idx, c["coo_cols"])
+        assert np.array_equal(csr.values, c["coo_vals"])
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_features_bit_exact(name):
+    c = case(name)
+    csr = P.convert(coo_of(c), P.FormatTag.CSR)
+    fv = P.extract_features(csr)
+    assert fv.to_array().tolist() == c["features"].tolist()
+
+
+def test_features_large_against_oracle():
+    for n, m, ptr, cols, vals in (G.powerlaw_spd(200000, seed=4), G.convdiff9(700),
+                                  G.laplace27(40)):
+        fv = P.extract_features(P.CsrMatrix(n, m, ptr, cols, vals))
+        assert fv.to_array().tolist() == O.features(O.OCsr(n, m, ptr, cols, vals))
+
+
+def test_feature_cancellation_and_counters():
+    n, m, ptr, cols, vals = G.poisson2d(40)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    ev = threading.Event()
+    ev.set()
+    cnt = TraversalCounter()
+    assert P.extract_features(csr, ev, counter=cnt) is None
+    assert cnt.col_idx_reads == 0 and cnt.row_ptr_reads == 0
+    cnt = TraversalCounter()
+    assert P.extract_features(csr, counter=cnt, row_chunk=64) is not None
+    assert cnt.col_idx_reads == csr.nnz
+    assert cnt.row_ptr_reads <= 2 * (csr.nrows + 1) + 2 * (csr.nrows // 64 + 1)
+
+    cancel = threading.Event()
+
+    class Tripping(TraversalCounter):
+        def __setattr__(self, k, v):
+            super().__setattr__(k, v)
+            if k == "col_idx_reads" and v > 0:
+                cancel.set()
+
+    assert P.extract_features(csr, cancel, counter=Tripping(), row_chunk=16) is None
+
+
+def test_device_stencil_generator_matches_host():
+    for dims, gen in (((30, 30), G.poisson2d(30)), ((25, 25), G.convdiff9(25)),
+                      ((9, 9, 9), G.laplace27(9))):
+        n, _, ptr, cols, vals = gen
+        offs, w = [], []
+        if len(dims) == 2 and vals.max() == 4.0:
+            offs, w = [(0, 0), (0, -1), (0, 1), (-1, 0), (1, 0)], [4.0, -1, -1, -1, -1]
+        elif len(dims) == 2:
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    offs.append((dy, dx))
+                    w.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
+        else:
+            for dz in (-1, 0, 1):
+                for dy in (-1, 0, 1):
+                    for dx in (-1, 0, 1):
+                        offs.append((dz, dy, dx))
+                        w.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+        dev = P.CsrMatrix.stencil(dims, offs, w)
+        assert dev.nnz == cols.size
+        assert np.array_equal(dev.row_ptr, ptr)
+        assert np.array_equal(dev.col_idx, cols)
+        assert np.array_equal(dev.values, vals)

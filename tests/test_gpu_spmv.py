@@ -1,0 +1,163 @@
+"""GPU parity: the 13 SpMV kernels against the reference's own outputs.
+
+Every deterministic configuration must be BIT-IDENTICAL to the golden y the
+reference produced (tests/golden, generated from /root/reference); COO/LibB
+(atomic scatter, nondeterministic in the reference too) is held to the
+reference's 1e-8 bar.  Larger matrices are checked against the CPU oracle
+bit-for-bit, fp32 against fp64 at fp32 tolerance.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from golden_io import case, case_names, spmv_keys
+
+import paper_2411_10143_b200 as P
+from paper_2411_10143_b200 import device, generators as G
+
+pytestmark = pytest.mark.gpu
+ATOMIC = P.SpmvConfig(P.FormatTag.COO, P.Library.LIB_B)
+
+
+def coo_of(c):
+    return P.CooMatrix(int(c["nrows"]), int(c["ncols"]), c["coo_rows"], c["coo_cols"], c["coo_vals"])
+
+
+def rel(got, want):
+    s = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (s if s else 1.0)
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_golden_bit_exact(name):
+    c = case(name)
+    coo = coo_of(c)
+    reps = {}
+    for tok, w in spmv_keys(c):
+        cfg = P.SpmvConfig.from_token(tok)
+        if cfg.format not in reps:
+            reps[cfg.format] = P.convert(coo, cfg.format)
+        got = P.execute_spmv(cfg, reps[cfg.format], c["x"], workers=w)
+        want = c[f"y|{tok}|{w}"]
+        assert np.array_equal(got, want), (tok, w, np.max(np.abs(got - want)))
+        # sign of zero included: the kernels mirror numpy's -0.0 handling too
+        assert np.array_equal(np.signbit(got), np.signbit(want)), (tok, w)
+    got = P.execute_spmv(ATOMIC, coo, c["x"])
+    assert rel(got, c["y_reference"]) <= 1e-8
+    csr = reps.get(P.FormatTag.CSR) or P.convert(coo, P.FormatTag.CSR)
+    assert np.array_equal(P.spmv_reference(csr, c["x"]), c["y_reference"])
+
+
+@pytest.mark.parametrize("gen", ["poisson", "convdiff", "powerlaw", "laplace27"])
+def test_larger_matrices_against_oracle(gen):
+    n, m, ptr, cols, vals = {
+        "poisson": lambda: G.poisson2d(300),
+        "convdiff": lambda: G.convdiff9(200),
+        "powerlaw": lambda: G.powerlaw_spd(60000, seed=7),
+        "laplace27": lambda: G.laplace27(30),
+    }[gen]()
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    ocsr = O.OCsr(n, m, ptr, cols, vals)
+    x = np.random.default_rng(11).uniform(-1.0, 1.0, size=m)
+    reps = {"CSR": ocsr, "COO": O.csr_to_coo(ocsr)}
+    for fmt in ("ELL", "DIA", "HYB"):
+        try:
+            reps[fmt] = O.convert(ocsr, fmt)
+        except O.OracleInapplicable:
+            pass
+    for cfg in P.enumerate_configs():
+        if cfg.format.value not in reps or cfg == ATOMIC:
+            continue
+        rep = P.convert(csr, cfg.format)
+        for w in ((1, 4, 148) if cfg.library is P.Library.LIB_C else (4,)):
+            got = P.execute_spmv(cfg, rep, x, workers=w)
+            want = O.spmv(cfg.token(), reps[cfg.format.value], x, workers=w)
+            assert np.array_equal(got, want), (cfg.token(), w)
+    got = P.execute_spmv(ATOMIC, P.convert(csr, P.FormatTag.COO), x)
+    assert rel(got, O.spmv_sequential(ocsr, x)) <= 1e-12
+
+
+def test_fp32_kernels_against_fp64():
+    n, m, ptr, cols, vals = G.powerlaw_spd(20000, seed=2)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    x = np.random.default_rng(5).uniform(0.5, 1.5, size=m)
+    s = device.thread_stream()
+    x32 = device.DeviceVector.from_numpy(x.astype(np.float32), s)
+    x64 = device.DeviceVector.from_numpy(x, s)
+    for cfg in P.enumerate_configs():
+        rep = P.convert(csr, cfg.format) if cfg.format is not P.FormatTag.DIA else None
+        if rep is None:
+            continue
+        y64 = P.execute_spmv(cfg, rep, x64, stream=s).to_numpy(s)
+        y32 = P.execute_spmv(cfg, rep, x32, stream=s).to_numpy(s)
+        assert y32.dtype == np.float32
+        assert rel(y32.astype(np.float64), y64) <= 1e-5, cfg.token()
+
+
+def test_device_buffer_path_matches_host_path():
+    n, m, ptr, cols, vals = G.convdiff9(64)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    x = np.random.default_rng(1).uniform(0.5, 1.5, size=m)
+    s = device.thread_stream()
+    xd = device.DeviceVector.from_numpy(x, s)
+    for cfg in P.enumerate_configs():
+        if cfg == ATOMIC:
+            continue
+        rep = P.convert(csr, cfg.format)
+        host = P.execute_spmv(cfg, rep, x)
+        dev = P.execute_spmv(cfg, rep, xd, stream=s).to_numpy(s)
+        assert np.array_equal(host, dev), cfg.token()
+
+
+def test_torch_tensor_interop():
+    torch = pytest.importorskip("torch")
+    n, m, ptr, cols, vals = G.poisson2d(50)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    x = torch.rand(m, dtype=torch.float64, device="cuda")
+    cfg = P.SpmvConfig(P.FormatTag.CSR, P.Library.LIB_A, 8)
+    y = P.execute_spmv(cfg, csr, x)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), P.execute_spmv(cfg, csr, x.cpu().numpy()))
+
+
+class TestContract:
+    def test_out_buffer_identity_and_refill(self):
+        csr = P.convert(P.CooMatrix(4, 4, np.arange(4), np.arange(4), np.ones(4)), P.FormatTag.CSR)
+        out = np.full(4, 7.0)
+        got = P.execute_spmv(P.SpmvConfig(P.FormatTag.CSR, P.Library.LIB_B), csr, np.ones(4),
+                             workers=2, out=out)
+        assert got is out and out.tolist() == [1.0] * 4
+
+    def test_format_mismatch(self):
+        coo = P.CooMatrix(3, 3, np.arange(3), np.arange(3), np.ones(3))
+        with pytest.raises(P.UnsupportedConfigError, match="expects"):
+            P.execute_spmv(P.SpmvConfig(P.FormatTag.CSR, P.Library.LIB_B), coo, np.ones(3))
+
+    def test_dimension_mismatch(self):
+        coo = P.CooMatrix(3, 3, np.arange(3), np.arange(3), np.ones(3))
+        with pytest.raises(ValueError, match="length"):
+            P.execute_spmv(P.DEFAULT_CONFIG, coo, np.ones(4))
+
+    def test_empty_matrix_all_configs(self):
+        coo = P.CooMatrix(4, 5, [], [], [])
+        for cfg in P.enumerate_configs():
+            y = P.execute_spmv(cfg, P.convert(coo, cfg.format), np.ones(5))
+            assert y.tolist() == [0.0] * 4, cfg.token()
+
+    def test_lane32_identity(self):
+        csr = P.convert(P.CooMatrix(3, 3, np.arange(3), np.arange(3), np.ones(3)), P.FormatTag.CSR)
+        got = P.execute_spmv(P.SpmvConfig(P.FormatTag.CSR, P.Library.LIB_A, 32), csr,
+                             np.array([1.0, 2.0, 3.0]))
+        assert got.tolist() == [1.0, 2.0, 3.0]
+
+    def test_determinism(self):
+        n, m, ptr, cols, vals = G.powerlaw_spd(30000, seed=9)
+        csr = P.CsrMatrix(n, m, ptr, cols, vals)
+        x = np.random.default_rng(2).uniform(0.5, 1.5, size=m)
+        for cfg in P.enumerate_configs():
+            if cfg == ATOMIC or cfg.format is P.FormatTag.DIA:
+                continue
+            rep = P.convert(csr, cfg.format)
+            a = P.execute_spmv(cfg, rep, x)
+            b = P.execute_spmv(cfg, rep, x)
+            assert np.array_equal(a, b), cfg.token()
