@@ -1,0 +1,431 @@
+"""Benchmark: GMRES(30) time-to-solution including preprocessing on B200.
+
+Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
+GMRES(30), fp64, tol 1e-8, b = A*1, on the nonsymmetric 9-point
+convection-diffusion matrix 2000x2000 (n = 4,000,000, nnz = 35,976,004).
+One step = one full async predict-while-solve (the paper's AsyGMRES): the
+solve starts at once on the default CSR-vector kernel (CSR/LibA/32) while
+the advisor stream extracts features, runs the shipped cascade models and
+converts to the predicted format; the solver swaps mid-solve.  Time to
+solution therefore includes all preprocessing.
+
+  value  — seconds per solve with the matrix and b resident in HBM
+  e2e    — the same solve through the public API from pinned HOST buffers:
+           CSR upload (H2D) inside the clock, solution download (D2H)
+  roofline — the dominant kernel group of the step, bytes per §8(d),
+           timed with CUDA events on the solver stream inside the timed steps
+  cpu_baseline — the reference algorithm (oracle port, bit-exact to the
+           reference) on the host cores, bounded sample (oracle/bench_cpu.py)
+
+`--impl reference` prints the reference arm (CPU oracle port) instead.
+Multi-GPU (torchrun): every rank solves its own replica (weak scaling; the
+row-partitioned solver is not in this round), value = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NX = 2000
+TOL = 1e-8
+RESTART = 30
+METRIC = "GMRES(30) time-to-solution incl. preprocessing (features+cascade+conversion)"
+WORKLOAD = (f"config2: GMRES({RESTART}) fp64, tol {TOL:g}, b=A*1, nonsymmetric 9-point "
+            f"convection-diffusion {NX}x{NX} (n={NX * NX:,}, nnz={(3 * NX - 2) ** 2:,}); async "
+            "predict-while-solve starting on CSR/LibA/32 with the reference's shipped cascade "
+            "models")
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle port on the host cores
+# ---------------------------------------------------------------------------
+def run_cpu_sample(steps: int, warmup: int, total_iters: int, iters: int = 8) -> dict:
+    env = dict(os.environ)
+    env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+    env.pop("CUDA_VISIBLE_DEVICES", None)
+    cmd = [sys.executable, "-m", "oracle.bench_cpu", "--nx", str(NX), "--iters", str(iters),
+           "--total-iters", str(total_iters), "--repeat", str(steps), "--warmup", str(warmup)]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr[-2000:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    r = run_cpu_sample(args.steps, args.warmup, args.total_iters)
+    line = {"metric": METRIC, "value": r["value"], "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"] * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "mode": "sequential predict-then-solve (CPU)"},
+            "cpu_baseline": {"value": r["value"], "unit": "s", "cores": r["cores"],
+                             "kind": r["kind"], "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "detail": {"phases": r["phases"], "values": r["values"], "config": r["config"],
+                       "wall_seconds": time.perf_counter() - t0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------
+class EventTimer:
+    """CUDA-event pairs around solver launches, recorded on the solver stream."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.streams = {}
+        self.open = {}
+        self.done = []
+        self.active = False
+
+    def _stream(self, h):
+        s = self.streams.get(h)
+        if s is None:
+            s = self.streams[h] = self.torch.cuda.ExternalStream(h)
+        return s
+
+    def begin(self, tag, h):
+        if not self.active:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self._stream(h))
+        self.open[tag] = ev
+
+    def end(self, tag, h):
+        if not self.active:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self._stream(h))
+        self.done.append((tag, self.open.pop(tag), ev))
+
+    def summary(self):
+        self.torch.cuda.synchronize()
+        out = {}
+        for tag, a, b in self.done:
+            out.setdefault(tag, []).append(a.elapsed_time(b))
+        return out
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-i", str(index), "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        loaded = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in loaded:
+            for k, name in enumerate(names):
+                if r[3 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(loaded[0][1]) if loaded else None,
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+def algorithmic_bytes(tag: str, info, n: int) -> float:
+    """Bytes per launch per SURVEY.md §8(d) (device layout: fp64 values,
+    int32 indices)."""
+    tok = tag.split(":", 1)[1]
+    fmt = tok.split("/")[0]
+    nnz, ncols = info["nnz"], n
+    if fmt == "CSR":
+        return 12 * nnz + 4 * (n + 1) + 8 * ncols + 8 * n
+    if fmt == "DIA":
+        return 8 * info["ndiag"] * n + 8 * ncols + 8 * n
+    if fmt == "ELL":
+        return 12 * n * info["width"] + 8 * ncols + 8 * n
+    if fmt == "HYB":
+        return 12 * n * info["width"] + 16 * info["spill"] + 8 * ncols + 16 * n
+    return 16 * nnz + 8 * ncols + 8 * n          # COO
+
+
+def mgs_bytes(n: int, j: int) -> float:
+    """One Arnoldi orthogonalisation at column j: dot0 reads V0,w (16n);
+    pass i=1..j reads w,V[i-1],V[i] and writes w (32n); final reads w,V[j],
+    writes w (24n)."""
+    return 16 * n + 32 * n * j + 24 * n
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+def b200_arm(args):
+    ws, rank, local = dist_env()
+    os.environ.setdefault("SPMVTUNE_DEVICE", str(local))
+    import numpy as np
+    import torch
+
+    import paper_2411_10143_b200 as P
+    from paper_2411_10143_b200 import _lib, device
+    from paper_2411_10143_b200.solver import DeviceOptions
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.lib()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    # --- inputs ------------------------------------------------------------
+    offs, wts = [], []
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            offs.append((dy, dx))
+            wts.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
+    A = P.CsrMatrix.stencil((NX, NX), offs, wts)              # generated in HBM
+    n = A.nrows
+    models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
+    params = P.GmresParams(restart_m=RESTART, tol=TOL, max_iters=1000)
+    start_cfg = P.GPU_DEFAULT_CONFIG
+    s = device.thread_stream()
+    ones = device.DeviceVector.from_numpy(np.ones(n), s)
+    b_dev = device.DeviceVector(n)
+    _lib.check(L.svb_spmv_sequential(A._device().handle, ones.ptr, b_dev.ptr, s.handle))  # b = A*1
+    s.sync()
+
+    def step(timer=None):
+        with DeviceOptions(timer=timer, keep_solution_on_device=True):
+            return P.async_solve(A, b_dev, params, models, initial_config=start_cfg)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # --- timed region (device-resident inputs) -----------------------------
+    timer = EventTimer()
+    timer.active = True
+    clocks = ClockSampler(local)
+    launches0 = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    t_ev0 = torch.cuda.Event(enable_timing=True)
+    t_ev1 = torch.cuda.Event(enable_timing=True)
+    per_step, reports = [], []
+    t_ev0.record()
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rep = step(timer)
+        per_step.append(time.perf_counter() - t0)
+        reports.append(rep)
+    torch.cuda.synchronize()
+    t_ev1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    barrier()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    dev_ms = t_ev0.elapsed_time(t_ev1)
+    # whole-region device time (events on the default stream bracket all work,
+    # the solve's own streams are synchronised inside each step)
+    total_s = max(dev_ms / 1e3, wall)
+    if ws > 1:
+        t = torch.tensor([total_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_s = float(t.item())
+    value = total_s / args.steps
+    kern = timer.summary()
+
+    # --- per-kernel roofline ----------------------------------------------------
+    hbm, peak_kind = peaks()
+    infos = {}
+    last = reports[-1]
+    for swap in last.config_timeline:
+        tok = swap.config.token()
+        rep = A if swap.config.format is P.FormatTag.CSR else P.convert(A, swap.config.format)
+        inf = rep._device().info
+        infos[tok] = {"nnz": int(inf.nnz), "ndiag": int(inf.ndiag), "width": int(inf.width),
+                      "spill": int(inf.spill_nnz)}
+    groups = {}
+    for tag, ms in kern.items():
+        tot = sum(ms)
+        if tag.startswith("spmv:"):
+            tok = tag.split(":", 1)[1]
+            if tok not in infos:
+                continue
+            byts = algorithmic_bytes(tag, infos[tok], n) * len(ms)
+        elif tag == "mgs":
+            # j cycles 0..restart-1 across steps; the column of each call is
+            # reconstructed from the iteration schedule of the reports
+            js = []
+            for r in reports:
+                js += [it % RESTART for it in range(r.iterations)]
+            byts = sum(mgs_bytes(n, j) for j in js[:len(ms)])
+        else:
+            continue
+        groups[tag] = {"launches": len(ms), "ms_total": tot, "ms_avg": tot / len(ms),
+                       "gbs": byts / (tot / 1e3) / 1e9, "bytes_per_launch": byts / len(ms)}
+    step_ms = value * 1e3
+    for g in groups.values():
+        g["share_of_step"] = g["ms_total"] / args.steps / step_ms
+    dom_tag = max(groups, key=lambda t: groups[t]["ms_total"]) if groups else None
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists() and dom_tag:
+        tr = json.loads(prof.read_text())
+        traffic = tr.get(dom_tag)
+    roofline = None
+    if dom_tag:
+        g = groups[dom_tag]
+        roofline = {"kernel": dom_tag, "bound": "hbm", "achieved": round(g["gbs"], 1),
+                    "peak": hbm, "unit": "GB/s", "frac": round(g["gbs"] / hbm, 4),
+                    "traffic": traffic, "peak_kind": peak_kind,
+                    "bytes_per_launch": g["bytes_per_launch"], "avg_launch_ms": g["ms_avg"]}
+
+    # --- end-to-end through the public API from pinned host buffers -----------------
+    e2e = None
+    if rank == 0 or ws > 1:
+        rp = np.asarray(A.row_ptr)
+        ci = np.asarray(A.col_idx)
+        vv = np.asarray(A.values)
+        bh = b_dev.to_numpy(s)
+        pin = {}
+        for k, arr in (("rp", rp), ("ci", ci), ("vv", vv), ("b", bh)):
+            t = torch.empty(arr.size, dtype=torch.from_numpy(arr[:1]).dtype, pin_memory=True)
+            t.numpy()[:] = arr
+            pin[k] = t
+        Ah = P.CsrMatrix(n, n, pin["rp"].numpy(), pin["ci"].numpy(), pin["vv"].numpy())
+        b_host = pin["b"].numpy()
+
+        def e2e_step():
+            Ah._dev = None                     # drop the device copy: upload inside the clock
+            rep = P.async_solve(Ah, b_host, params, models, initial_config=start_cfg)
+            return rep
+        e2e_step()
+        torch.cuda.synchronize()
+        k_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            rep_e = e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / k_e2e
+        h2d = rp.nbytes + ci.nbytes + vv.nbytes + bh.nbytes
+        d2h = rep_e.solution.nbytes + 48 * (rep_e.iterations + 4)
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
+               "note": "CsrMatrix from pinned host int64/f64 arrays (upload + narrowing inside "
+                       "the clock) -> async_solve -> solution to host"}
+
+    # --- comparison solves (not timed as `value`) ---------------------------
+    detail = {}
+    if rank == 0:
+        with DeviceOptions(keep_solution_on_device=True):
+            t0 = time.perf_counter()
+            d = P.gmres_solve(A, b_dev, params, initial_config=start_cfg)
+            torch.cuda.synchronize()
+            detail["default_csr_vector_gpu_s"] = time.perf_counter() - t0
+            detail["default_iterations"] = d.iterations
+            t0 = time.perf_counter()
+            sq = P.sequential_predict_solve(A, b_dev, params, models)
+            torch.cuda.synchronize()
+            detail["sequential_gpu_s"] = time.perf_counter() - t0
+            detail["sequential_phases"] = sq.phases
+    detail.update({
+        "iterations": last.iterations, "converged": last.converged,
+        "final_residual": last.final_residual,
+        "timeline": [sw.to_dict() for sw in last.config_timeline],
+        "advisor_outcome": last.advisor_outcome, "per_step_wall_s": per_step,
+        "device_region_ms": dev_ms, "wall_region_s": wall, "kernels": groups})
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            r = run_cpu_sample(1, 0, last.iterations)
+            cpu = {"value": r["value"], "unit": "s", "cores": r["cores"], "kind": r["kind"],
+                   "sample": r["sample"], "phases": r["phases"]}
+        except Exception as exc:  # measurement must not kill the bench line
+            cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"[:300]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "mode": "async",
+                           "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                           "l2": "inputs larger than L2 (CSR 448 MB + Krylov basis 992 MB vs 126 MB L2)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk, "detail": detail}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--total-iters", type=int, default=77,
+                    help="reference arm: GMRES iterations the solve takes (77 at config 2)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args(argv)
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("--steps >= 1 and --warmup >= 0")
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -86,6 +86,8 @@ typedef enum {
 /* ---- library ------------------------------------------------------------ */
 const char* svb_last_error(void);
 int svb_abi_version(void);
+/* Number of this library's kernels launched so far by the process. */
+int svb_launch_count(int64_t* out);
 /* Select the device for the calling thread and warm the allocator. */
 int svb_init(int device);
 /* Block until `stream` drains (used by host wrappers at API boundaries). */

@@ -1,0 +1,125 @@
+"""CPU reference timing for bench.py — TEST/MEASUREMENT INFRASTRUCTURE ONLY.
+
+Times the reference algorithm (this package's numpy restatement, pinned
+bit-exact to /root/reference by tests/test_oracle_golden.py) on the GPU
+box's host cores, for the bench workload: the reference's predict-then-solve
+flow (solver.py:496-540) — features -> cascade (shipped models) -> format
+conversion -> restarted GMRES — on the 9-point convection-diffusion matrix.
+
+A full CPU solve takes ~30 s, so each sample runs the whole
+preprocessing plus ``iters`` GMRES iterations at full size and extrapolates
+the solve to ``total_iters`` iterations (stated in the output "sample").
+
+    python -m oracle.bench_cpu --nx 2000 --iters 4 --total-iters 77 --repeat 1
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+from . import cpu_oracle as O
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def convdiff9_csr(nx: int, diag: float = 8.5, beta: float = 0.25) -> O.OCsr:
+    """Same structure as paper_2411_10143_b200.generators.convdiff9 (restated
+    here so the oracle never imports the product)."""
+    n = nx * nx
+    y, x = np.divmod(np.arange(n, dtype=np.int64), nx)
+    cols, vals, masks = [], [], []
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            ok = (x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < nx)
+            masks.append(ok)
+            cols.append(np.arange(n, dtype=np.int64) + dy * nx + dx)
+            vals.append(diag if (dx, dy) == (0, 0) else -1.0 - beta * (dx + dy))
+    masks = np.stack(masks)
+    lens = masks.sum(axis=0)
+    ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    c2 = np.stack(cols)
+    v2 = np.broadcast_to(np.asarray(vals)[:, None], masks.shape)
+    return O.OCsr(n, n, ptr, c2.T[masks.T], np.ascontiguousarray(v2.T[masks.T]))
+
+
+def load_models():
+    d = ROOT / "tests" / "golden" / "models"
+    return {p.stem: json.loads(p.read_text()) for p in d.glob("*.json")}
+
+
+def sample(csr: O.OCsr, models, iters: int, total_iters: int, b: np.ndarray) -> dict:
+    """One bounded sample of the predict-then-solve pipeline."""
+    t = {}
+    t0 = time.perf_counter()
+    coo = O.csr_to_coo(csr)                      # the user's matrix arrives as COO
+    t["to_csr"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fv = O.features(O.coo_to_csr(coo))
+    t["features"] = time.perf_counter() - t0 + t["to_csr"]
+    t0 = time.perf_counter()
+    final = O.cascade(models, fv)[-1]
+    t["inference"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fmt = final.split("/")[0]
+    rep = O.convert(coo, fmt)
+    t["conversion"] = time.perf_counter() - t0
+    # per-iteration times of Arnoldi steps j = 0..iters-1; step j costs one
+    # SpMV plus j+1 MGS dot/axpy pairs, so t_j = a + b*j is fitted and summed
+    # over the restart schedule of `total_iters` iterations (restart 30)
+    marks = [time.perf_counter()]
+    res = O.gmres(lambda v: O.spmv(final, rep, v, workers=4), b, restart=30, tol=1e-300,
+                  max_iters=iters, on_iteration=lambda done, j: marks.append(time.perf_counter()))
+    # the first step of a cycle also carries the restart (explicit residual,
+    # basis allocation), so it is taken as measured and the fit uses j >= 1
+    tj = np.diff(np.asarray(marks))
+    js = np.arange(tj.size)
+    first = float(tj[0])
+    slope, icpt = np.polyfit(js[1:], tj[1:], 1) if tj.size >= 3 else (0.0, float(tj[-1]))
+    sched = np.arange(total_iters) % 30
+    t["solve_extrapolated"] = float(np.sum(np.where(sched == 0, first, icpt + slope * sched)))
+    prep = t["features"] + t["inference"] + t["conversion"]
+    return {"value": prep + t["solve_extrapolated"], "phases": t, "config": final,
+            "per_iteration_s": float(np.mean(icpt + slope * sched)),
+            "sampled_iterations": res["iterations"], "fit": [float(icpt), float(slope)]}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nx", type=int, default=2000)
+    ap.add_argument("--iters", type=int, default=4)
+    ap.add_argument("--total-iters", type=int, default=77)
+    ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=0)
+    a = ap.parse_args(argv)
+    t_gen = time.perf_counter()
+    csr = convdiff9_csr(a.nx)
+    b = O.spmv_sequential(csr, np.ones(csr.nrows))        # RHS outside the clock (solver.py:355)
+    models = load_models()
+    t_gen = time.perf_counter() - t_gen
+    for _ in range(a.warmup):
+        sample(csr, models, a.iters, a.total_iters, b)
+    runs = [sample(csr, models, a.iters, a.total_iters, b) for _ in range(a.repeat)]
+    vals = sorted(r["value"] for r in runs)
+    out = {"value": vals[len(vals) // 2], "values": [r["value"] for r in runs],
+           "unit": "s", "cores": os.cpu_count(),
+           "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
+           "kind": "port",
+           "sample": (f"reference predict-then-solve on conv-diff9 {a.nx}^2 "
+                      f"(n={csr.nrows}, nnz={csr.cols.size}): features+cascade+conversion "
+                      f"in full, {runs[0]['sampled_iterations']} GMRES(30) iterations timed "
+                      f"and extrapolated to {a.total_iters}"),
+           "phases": runs[len(runs) // 2]["phases"], "config": runs[0]["config"],
+           "per_iteration_s": runs[len(runs) // 2]["per_iteration_s"],
+           "setup_seconds": t_gen}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -483,7 +483,7 @@ def _back_substitute(H, g, j, V):
     return V[:j + 1].T @ y
 
 
-def gmres(matvec, b, restart=30, tol=1e-8, max_iters=1000) -> dict:
+def gmres(matvec, b, restart=30, tol=1e-8, max_iters=1000, on_iteration=None) -> dict:
     """Restarted MGS-GMRES with Givens rotations and explicit-residual
     confirmation, restating solver.py:219-342 without the mailbox.
 
@@ -546,6 +546,8 @@ def gmres(matvec, b, restart=30, tol=1e-8, max_iters=1000) -> dict:
             if not math.isfinite(est):
                 return out(False, None, "nonfinite")
             hist.append(est)
+            if on_iteration is not None:
+                on_iteration(done, j)
             if hn == 0.0:
                 if H[j, j] != 0.0:
                     x = x + _back_substitute(H, g, j, V)

@@ -48,6 +48,7 @@ class KrylovStatus(C.Structure):
 _SIGS = {
     "svb_last_error": [],
     "svb_abi_version": [],
+    "svb_launch_count": [_PI64],
     "svb_init": [C.c_int],
     "svb_stream_sync": [_P],
     "svb_stream_create": [C.c_int, _PP],
@@ -139,6 +140,12 @@ def lib():
                 check(L.svb_init(dev))
                 _initialised = True
     return L
+
+
+def launch_count() -> int:
+    n = C.c_int64()
+    load().svb_launch_count(C.byref(n))
+    return n.value
 
 
 def last_error() -> str:

@@ -38,7 +38,15 @@ struct Error {
     }                                                                        \
   } while (0)
 
-#define SVB_CHECK_LAUNCH() SVB_CUDA_TRY(cudaGetLastError())
+// Every launch of one of this library's kernels is counted (svb_launch_count):
+// bench.py reports the count for its timed region as evidence that the
+// native path ran.
+void note_launches(int64_t n);
+#define SVB_CHECK_LAUNCH()                 \
+  do {                                     \
+    ::svb::note_launches(1);               \
+    SVB_CUDA_TRY(cudaGetLastError());      \
+  } while (0)
 
 #define SVB_REQUIRE(cond, code, msg)                \
   do {                                                \

@@ -483,7 +483,7 @@ int svb_convert(const svb_matrix* src, int target, int64_t max_ell_cells, void* 
       default: m = build_hyb(v, s); break;
     }
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 

@@ -124,6 +124,6 @@ extern "C" int svb_csr_stencil(int ndim, const int64_t* dims, int nst, const int
       narrow_i64_to_i32(ptr<int64_t>(ptr64), ptr<int32_t>(m->ptr), n + 1, s);
     }
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }

@@ -543,6 +543,7 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
     k_gm_dot0<<<k->rgrid, KB, 0, s>>>(G, j);
     for (int i = 1; i <= j; ++i) k_gm_pass<<<k->rgrid, KB, 0, s>>>(G, i, j);
     k_gm_final<<<k->rgrid, KB, 0, s>>>(G, j, bnorm);
+    note_launches(j + 1);
     SVB_CHECK_LAUNCH();
   });
 }
@@ -560,6 +561,7 @@ int svb_gmres_update_x(svb_krylov* k, int32_t j, void* stream) {
     Gm G = gm_of(k);
     k_gm_solve_y<<<1, 32, 0, S(stream)>>>(G, j);
     k_gm_update_x<<<k->rgrid, KB, 0, S(stream)>>>(G, j, ptr<double>(k->x));
+    note_launches(1);
     SVB_CHECK_LAUNCH();
   });
 }
@@ -583,6 +585,7 @@ int svb_cg_step(svb_krylov* k, double bnorm, void* stream) {
     k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
                                          ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev);
     k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal));
+    note_launches(2);
     SVB_CHECK_LAUNCH();
   });
 }

@@ -18,6 +18,9 @@ static thread_local std::string tls_error;
 void set_error(const std::string& msg) { tls_error = msg; }
 const char* get_error() { return tls_error.c_str(); }
 
+static std::atomic<int64_t> g_launches{0};
+void note_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 DevBuf::~DevBuf() {
   if (ptr) cudaFreeAsync(ptr, stream);
 }
@@ -105,12 +108,16 @@ const float* vals_f32(const svb_matrix* m, cudaStream_t s) {
   if (!m->vals32) {
     int64_t n = m->vals ? (int64_t)(m->vals->bytes / 8) : 0;
     m->vals32 = to_f32(m->vals, n, s);
+    detach(m->vals32);
   }
   return ptr<float>(m->vals32);
 }
 const float* svals_f32(const svb_matrix* m, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(m->mu);
-  if (!m->svals32) m->svals32 = to_f32(m->svals, m->spill_nnz, s);
+  if (!m->svals32) {
+    m->svals32 = to_f32(m->svals, m->spill_nnz, s);
+    detach(m->svals32);
+  }
   return ptr<float>(m->svals32);
 }
 
@@ -200,6 +207,10 @@ static Buf upload_i32(const int64_t* host, int64_t n, cudaStream_t s) {
 extern "C" {
 
 const char* svb_last_error(void) { return get_error(); }
+int svb_launch_count(int64_t* out) {
+  *out = g_launches.load();
+  return SVB_OK;
+}
 int svb_abi_version(void) { return SVB_ABI_VERSION; }
 
 int svb_init(int device) {
@@ -310,7 +321,7 @@ int svb_coo_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
     m->cols = upload_i32(cols_host, nnz, s);
     m->vals = upload(vals_host, nnz * 8, s);
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 
@@ -329,7 +340,7 @@ int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
     m->cols = upload_i32(col_idx_host, nnz, s);
     m->vals = upload(vals_host, nnz * 8, s);
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 
@@ -348,7 +359,7 @@ int svb_ell_create(int64_t nrows, int64_t ncols, int64_t width, const int64_t* c
     for (int64_t i = 0; i < cells; ++i) stored += cols_host[i] != ncols;
     m->nnz = stored;
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 
@@ -371,7 +382,7 @@ int svb_dia_create(int64_t nrows, int64_t ncols, int64_t ndiag, const int64_t* o
     }
     m->nnz = stored;
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 
@@ -391,7 +402,7 @@ int svb_hyb_create(const svb_matrix* ell, const svb_matrix* coo, void* stream, s
     m->nnz = ell->nnz + coo->nnz;
     m->ptr = rows_to_ptr(ptr<int32_t>(coo->rows), coo->nnz, coo->nrows, true, s);
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = m;
+    *out = publish(m);
   });
 }
 

@@ -42,6 +42,17 @@ struct svb_matrix {
 
 namespace svb {
 
+// Long-lived buffers are freed on the legacy stream after a device-wide sync
+// (svb_matrix_destroy), never on the stream that allocated them: that stream
+// may belong to a thread (the advisor) that is gone by then.
+inline void detach(Buf& b) {
+  if (b) b->stream = 0;
+}
+inline svb_matrix* publish(svb_matrix* m) {
+  for (Buf* b : {&m->ptr, &m->rows, &m->cols, &m->vals, &m->offs, &m->scols, &m->svals}) detach(*b);
+  return m;
+}
+
 // fp32 copies of vals / svals, created on first use on `s`
 const float* vals_f32(const svb_matrix* m, cudaStream_t s);
 const float* svals_f32(const svb_matrix* m, cudaStream_t s);

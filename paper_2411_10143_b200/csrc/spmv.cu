@@ -391,6 +391,7 @@ static const int64_t* device_bounds(const svb_matrix* m, int64_t workers, int* n
   Buf b = alloc(h.size() * 8, s);
   SVB_CUDA_TRY(cudaMemcpyAsync(b->ptr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
   SVB_CUDA_TRY(cudaStreamSynchronize(s));  // h is a host temporary
+  detach(b);
   c.map[key] = b;
   return ptr<int64_t>(b);
 }
