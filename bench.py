@@ -24,6 +24,7 @@ row-partitioned solver is not in this round), value = max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -139,6 +140,56 @@ class EventTimer:
         return out
 
 
+class NvmlClockSampler:
+    """In-process NVML sampling of SM clock and throttle reasons during the
+    timed region.  (An `nvidia-smi -lms` child process holds driver locks
+    long enough to stall CUDA API calls by tens of ms; NVML reads are cheap.)"""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period: float = 0.25):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.period = period
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+        self.samples.append((sm, reasons, util))
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
+
+    def stop(self) -> dict:
+        self.stop_ev.set()
+        self.t.join()
+        try:
+            self._sample()
+        except Exception:
+            pass
+        loaded = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = sorted({name for s in loaded for name, bit in self.REASONS.items() if s[1] & bit})
+        sm = [s[0] for s in loaded]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "samples_under_load": len(loaded),
+                "source": "nvml"}
+
+
 class ClockSampler:
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -250,26 +301,30 @@ def b200_arm(args):
     torch.cuda.synchronize()
 
     # --- timed region (device-resident inputs) -----------------------------
-    timer = EventTimer()
-    timer.active = True
-    clocks = ClockSampler(local)
+    try:
+        clocks = NvmlClockSampler(local)
+    except Exception:
+        clocks = ClockSampler(local)
     launches0 = _lib.launch_count()
     barrier()
     torch.cuda.synchronize()
     t_ev0 = torch.cuda.Event(enable_timing=True)
     t_ev1 = torch.cuda.Event(enable_timing=True)
     per_step, reports = [], []
+    gc.collect()
+    gc.disable()      # no cyclic-GC pauses inside the timed steps
     t_ev0.record()
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        rep = step(timer)
+        rep = step()
         per_step.append(time.perf_counter() - t0)
         reports.append(rep)
     torch.cuda.synchronize()
     t_ev1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
+    gc.enable()
     barrier()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
@@ -282,6 +337,14 @@ def b200_arm(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_s = float(t.item())
     value = total_s / args.steps
+
+    # --- kernel timing: separate instrumented steps (CUDA events around every
+    # SpMV and Arnoldi launch on the solver stream); kept out of `value`
+    # because recording events per launch adds host work to the step
+    timer = EventTimer()
+    timer.active = True
+    prof_steps = max(1, min(args.steps, 3))
+    prof_reports = [step(timer) for _ in range(prof_steps)]
     kern = timer.summary()
 
     # --- per-kernel roofline ----------------------------------------------------
@@ -306,7 +369,7 @@ def b200_arm(args):
             # j cycles 0..restart-1 across steps; the column of each call is
             # reconstructed from the iteration schedule of the reports
             js = []
-            for r in reports:
+            for r in prof_reports:
                 js += [it % RESTART for it in range(r.iterations)]
             byts = sum(mgs_bytes(n, j) for j in js[:len(ms)])
         else:
@@ -315,7 +378,7 @@ def b200_arm(args):
                        "gbs": byts / (tot / 1e3) / 1e9, "bytes_per_launch": byts / len(ms)}
     step_ms = value * 1e3
     for g in groups.values():
-        g["share_of_step"] = g["ms_total"] / args.steps / step_ms
+        g["share_of_step"] = g["ms_total"] / prof_steps / step_ms
     dom_tag = max(groups, key=lambda t: groups[t]["ms_total"]) if groups else None
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
@@ -383,6 +446,8 @@ def b200_arm(args):
         "final_residual": last.final_residual,
         "timeline": [sw.to_dict() for sw in last.config_timeline],
         "advisor_outcome": last.advisor_outcome, "per_step_wall_s": per_step,
+        "per_step_swaps": [[(sw.iteration, sw.config.token(), round(sw.swap_cost_seconds, 5))
+                            for sw in r.config_timeline] for r in reports],
         "device_region_ms": dev_ms, "wall_region_s": wall, "kernels": groups})
 
     cpu = None

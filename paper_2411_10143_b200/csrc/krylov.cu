@@ -9,6 +9,8 @@
 // device inside an iteration, and the host reads one mapped status block
 // per iteration.  The modified Gram-Schmidt loop is fused as
 // "axpy_{i-1} + dot_i" passes: pass i reads w, V[i-1] and V[i] once.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstring>
 
@@ -22,7 +24,20 @@ struct svb_krylov {
   svb::Buf H, cs, sn, g, y, scal, partials, counter;
   svb_krylov_status* st_host = nullptr;
   svb_krylov_status* st_dev = nullptr;
+  // SM-resident MGS (k_gm_mgs_resident): rows per CTA, dynamic smem bytes,
+  // per-CTA partial slots; `normalized` = column whose V[j+1] the fused
+  // kernel already normalised
+  int64_t chunk = 0;
+  size_t res_smem = 0;
+  bool resident = false;
+  int normalized = -1;
+  svb::Buf gparts;
+  // recorded right after every status-producing kernel: the host waits on
+  // this, not on the stream, so work enqueued behind it (the speculative
+  // next SpMV, CG's p update) overlaps the host's decision
+  cudaEvent_t ev = nullptr;
   ~svb_krylov() {
+    if (ev) cudaEventDestroy(ev);
     if (st_host) cudaFreeHost(st_host);
   }
 };
@@ -263,6 +278,230 @@ __global__ void __launch_bounds__(KB) k_gm_final(Gm G, int j, double bnorm) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// SM-resident MGS: one persistent cooperative kernel per Arnoldi step.
+// CTA c (one per SM) owns rows [c*chunk, (c+1)*chunk) and keeps its slice of
+// w in shared memory for the whole orthogonalisation, so every pass streams
+// only the basis rows: w never round-trips through L2/HBM.  Passes are
+// separated by grid barriers; each CTA folds the per-CTA partials of a dot
+// product in the same fixed order, so every CTA holds the identical h_i
+// without a second barrier.  The final pass also normalises V[j+1] and CTA 0
+// runs the Givens epilogue.
+// ---------------------------------------------------------------------------
+constexpr int PB = 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order CTA sum, result returned to every thread
+__device__ __forceinline__ double cta_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < (PB / 32) ? scratch[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) scratch[32] = t;
+  }
+  __syncthreads();
+  const double r = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+// grid-wide fixed-order sum of one partial per CTA (double-buffered slots)
+__device__ __forceinline__ double grid_sum(double part, double* gparts, int slot, double* scratch,
+                                           cooperative_groups::grid_group& grid) {
+  if (threadIdx.x == 0) gparts[slot * gridDim.x + blockIdx.x] = part;
+  grid.sync();
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) t += __ldcg(gparts + slot * gridDim.x + b);
+    t = warp_sum(t);
+    if (threadIdx.x == 0) scratch[33] = t;
+  }
+  __syncthreads();
+  const double r = scratch[33];
+  __syncthreads();
+  return r;
+}
+
+// Lean CTA+grid reduction for the resident MGS kernel: two block barriers
+// per pass.  Warp partials go to shared memory; warp 0 folds them, publishes
+// the CTA partial, arrives on a monotonic grid counter (zeroed by the host
+// before the launch) and spins until all CTAs of this pass arrived, then
+// folds the per-CTA partials in fixed order.  Every CTA computes the same
+// total, so no broadcast barrier is needed.
+__device__ __forceinline__ double fused_grid_sum(double v, double* gparts, unsigned* counter, int pass,
+                                                 double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < (PB / 32) ? scratch[lane] : 0.0;
+    t = warp_sum(t);
+    const int slot = pass & 1;
+    if (lane == 0) {
+      gparts[slot * gridDim.x + blockIdx.x] = t;
+      __threadfence();
+      atomicAdd(counter, 1u);
+      const unsigned target = (unsigned)(pass + 1) * gridDim.x;
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+      } while (seen < target);
+    }
+    __syncwarp();
+    __threadfence();
+    double g = 0.0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) g += __ldcg(gparts + slot * gridDim.x + b);
+    g = warp_sum(g);
+    if (lane == 0) scratch[32 + slot] = g;
+  }
+  __syncthreads();
+  return scratch[32 + (pass & 1)];
+}
+
+__device__ void givens_epilogue(Gm& G, int j, double hnext, double bnorm) {
+  const int m = G.m;
+  double* H = G.H;
+  for (int i = 0; i < j; ++i) {
+    const double a = H[i * m + j], b = H[(i + 1) * m + j];
+    const double hi = G.cs[i] * a + G.sn[i] * b;
+    H[(i + 1) * m + j] = -G.sn[i] * a + G.cs[i] * b;
+    H[i * m + j] = hi;
+  }
+  const double hjj = H[j * m + j];
+  const double denom = hypot(hjj, hnext);
+  double c = 1.0, s = 0.0;
+  if (denom != 0.0) {
+    c = hjj / denom;
+    s = hnext / denom;
+  }
+  G.cs[j] = c;
+  G.sn[j] = s;
+  H[j * m + j] = c * hjj + s * hnext;
+  G.g[j + 1] = -s * G.g[j];
+  G.g[j] = c * G.g[j];
+  H[(j + 1) * m + j] = hnext;
+  const double est = fabs(G.g[j + 1]) / bnorm;
+  G.st->hnext = hnext;
+  G.st->hjj = H[j * m + j];
+  G.st->estimate = est;
+  G.st->nonfinite = bad(hnext) || bad(est);
+}
+
+// Bulk L2 prefetch (TMA engine, cp.async.bulk.prefetch.L2) of this CTA's
+// slice of the basis row the NEXT pass reads: the DRAM stream for pass i+1
+// overlaps pass i's arithmetic and grid barrier, so pass loads hit L2.
+__device__ __forceinline__ void prefetch_slice_l2(const double* p, int len) {
+  const char* base = reinterpret_cast<const char*>(p);
+  const int64_t bytes = ((int64_t)len * 8) & ~int64_t(15);
+  constexpr int64_t PIECE = 16384;
+  for (int64_t off = (int64_t)threadIdx.x * PIECE; off < bytes; off += PIECE * PB) {
+    const uint32_t sz = (uint32_t)(bytes - off < PIECE ? bytes - off : PIECE);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(sz) : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(PB, 1) k_gm_mgs_resident(Gm G, int j, double bnorm, int64_t chunk,
+                                                          double* gparts, unsigned* gcounter) {
+  extern __shared__ double ws[];
+  double* scratch = ws + chunk;  // 34 doubles
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = G.n < lo + chunk ? G.n : lo + chunk;
+  const int len = hi > lo ? (int)(hi - lo) : 0;
+  double* wg = G.V + (int64_t)(j + 1) * G.ld + lo;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+
+  // Loads are issued in batches of U per thread before any shared-memory
+  // update, so U independent 8-byte loads per operand stay in flight (the
+  // basis rows are read-only here: V[j+1] is written only after the last
+  // read).  Elements k = tid + u*PB keep every warp access coalesced.
+  constexpr int U = 8;
+  // pass 0: stage w, h_0 = V_0 . w
+  double acc = 0.0;
+  if (j >= 1) prefetch_slice_l2(G.V + G.ld + lo, len);
+  {
+    const double* v0 = G.V + lo;
+    for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
+      double a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        a[u] = k < len ? __ldcs(wg + k) : 0.0;
+        b[u] = k < len ? __ldcg(v0 + k) : 0.0;   // reused next pass: keep in L2
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        if (k < len) ws[k] = a[u];
+        acc += b[u] * a[u];
+      }
+    }
+  }
+  double h = fused_grid_sum(acc, gparts, gcounter, 0, scratch);
+  if (lead) G.H[j] = h;
+  // passes 1..j: w -= h_{i-1} V_{i-1};  h_i = V_i . w
+  for (int i = 1; i <= j; ++i) {
+    const double* vp = G.V + (int64_t)(i - 1) * G.ld + lo;
+    const double* vi = G.V + (int64_t)i * G.ld + lo;
+    if (i + 1 <= j) prefetch_slice_l2(G.V + (int64_t)(i + 1) * G.ld + lo, len);
+    acc = 0.0;
+    for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
+      double a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        a[u] = k < len ? __ldcs(vp + k) : 0.0;   // second and last use (L2 hit)
+        b[u] = k < len ? __ldcg(vi + k) : 0.0;   // reused next pass: keep in L2
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        if (k < len) {
+          const double w = ws[k] - h * a[u];
+          ws[k] = w;
+          acc += b[u] * w;
+        }
+      }
+    }
+    h = fused_grid_sum(acc, gparts, gcounter, i, scratch);
+    if (lead) G.H[i * G.m + j] = h;
+  }
+  // final: w -= h_j V_j; hnext = ||w||; V[j+1] = w / hnext
+  {
+    const double* vj = G.V + (int64_t)j * G.ld + lo;
+    acc = 0.0;
+    for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        a[u] = k < len ? __ldcs(vj + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * PB;
+        if (k < len) {
+          const double w = ws[k] - h * a[u];
+          ws[k] = w;
+          acc += w * w;
+        }
+      }
+    }
+  }
+  const double hnext = sqrt(fused_grid_sum(acc, gparts, gcounter, j + 1, scratch));
+#pragma unroll 4
+  for (int k = threadIdx.x; k < len; k += PB) wg[k] = ws[k] / hnext;
+  if (lead) givens_epilogue(G, j, hnext, bnorm);
+}
+
 // back-substitution of the rotated system (solver.py:211-214), one thread
 __global__ void k_gm_solve_y(Gm G, int j) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -464,6 +703,28 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
     k->counter = alloc(8, s);
     SVB_CUDA_TRY(cudaMemsetAsync(k->counter->ptr, 0, 8, s));
     SVB_CUDA_TRY(cudaMemsetAsync(k->x->ptr, 0, k->ld * 8, s));
+    // SM-resident MGS when every CTA's slice of w fits in shared memory
+    {
+      int dev = 0, optin = 0, coop = 0;
+      SVB_CUDA_TRY(cudaGetDevice(&dev));
+      SVB_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      SVB_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+      const int G = sm_count();
+      k->chunk = (((n + G - 1) / G) + 1) & ~int64_t(1);
+      k->res_smem = (size_t)(k->chunk + 34) * sizeof(double);
+      const char* mode = std::getenv("SPMVTUNE_MGS");
+      const bool allowed = !(mode && std::strcmp(mode, "stream") == 0);
+      if (allowed && coop && m >= 1 && k->res_smem <= (size_t)optin) {
+        SVB_CUDA_TRY(cudaFuncSetAttribute(k_gm_mgs_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)k->res_smem));
+        int per_sm = 0;
+        SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gm_mgs_resident, PB,
+                                                                   k->res_smem));
+        k->resident = per_sm >= 1;
+        k->gparts = alloc(2 * G * sizeof(double) + 64, s);   // + grid counter
+      }
+    }
+    SVB_CUDA_TRY(cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming));
     SVB_CUDA_TRY(cudaHostAlloc((void**)&k->st_host, sizeof(svb_krylov_status), cudaHostAllocMapped));
     std::memset(k->st_host, 0, sizeof(svb_krylov_status));
     SVB_CUDA_TRY(cudaHostGetDevicePointer((void**)&k->st_dev, k->st_host, 0));
@@ -499,9 +760,12 @@ int svb_krylov_vec(svb_krylov* k, int which, double** out) {
   });
 }
 
+static void mark(svb_krylov* k, cudaStream_t s) { SVB_CUDA_TRY(cudaEventRecord(k->ev, s)); }
+
 int svb_krylov_status_get(svb_krylov* k, void* stream, svb_krylov_status* out) {
   return guard([&] {
-    SVB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    (void)stream;
+    SVB_CUDA_TRY(cudaEventSynchronize(k->ev));
     std::atomic_thread_fence(std::memory_order_seq_cst);
     std::memcpy(out, (const void*)k->st_host, sizeof(svb_krylov_status));
   });
@@ -512,6 +776,7 @@ int svb_krylov_bnorm(svb_krylov* k, void* stream) {
     k_resnorm<<<k->rgrid, KB, 0, S(stream)>>>(ptr<double>(k->b), nullptr, k->n, ptr<double>(k->partials),
                                                ptr<unsigned>(k->counter), k->st_dev);
     SVB_CHECK_LAUNCH();
+    mark(k, S(stream));
   });
 }
 
@@ -521,15 +786,18 @@ int svb_krylov_residual(svb_krylov* k, void* stream) {
                                                ptr<double>(k->partials), ptr<unsigned>(k->counter),
                                                k->st_dev);
     SVB_CHECK_LAUNCH();
+    mark(k, S(stream));
   });
 }
 
 int svb_gmres_restart(svb_krylov* k, void* stream) {
   return guard([&] {
     SVB_REQUIRE(k->m >= 1, SVB_INVALID, "GMRES workspace needs restart m >= 1");
+    k->normalized = -1;
     Gm G = gm_of(k);
     k_gm_residual<<<k->rgrid, KB, 0, S(stream)>>>(G, ptr<double>(k->b), ptr<double>(k->tmp));
     SVB_CHECK_LAUNCH();
+    mark(k, S(stream));
     k_gm_scale<<<k->rgrid, KB, 0, S(stream)>>>(G.V, k->n, G.g);
     SVB_CHECK_LAUNCH();
   });
@@ -540,19 +808,36 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
     SVB_REQUIRE(j >= 0 && j < k->m, SVB_INVALID, "Arnoldi column out of range");
     Gm G = gm_of(k);
     cudaStream_t s = S(stream);
+    if (k->resident) {
+      int64_t chunk = k->chunk;
+      double* gp = ptr<double>(k->gparts);
+      unsigned* gc = reinterpret_cast<unsigned*>(gp + 2 * sm_count());
+      SVB_CUDA_TRY(cudaMemsetAsync(gc, 0, sizeof(unsigned), s));
+      void* args[] = {&G, &j, &bnorm, &chunk, &gp, &gc};
+      SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_gm_mgs_resident, dim3(sm_count()), dim3(PB),
+                                               args, k->res_smem, s));
+      note_launches(1);
+      k->normalized = j;
+      mark(k, s);
+      return;
+    }
+    k->normalized = -1;
     k_gm_dot0<<<k->rgrid, KB, 0, s>>>(G, j);
     for (int i = 1; i <= j; ++i) k_gm_pass<<<k->rgrid, KB, 0, s>>>(G, i, j);
     k_gm_final<<<k->rgrid, KB, 0, s>>>(G, j, bnorm);
     note_launches(j + 1);
     SVB_CHECK_LAUNCH();
+    mark(k, s);
   });
 }
 
 int svb_gmres_normalize(svb_krylov* k, int32_t j, void* stream) {
   return guard([&] {
+    if (k->normalized == j) return;  // already done (resident MGS kernel or an earlier call)
     Gm G = gm_of(k);
     k_gm_scale<<<k->rgrid, KB, 0, S(stream)>>>(G.V + (int64_t)(j + 1) * G.ld, k->n, G.H + (j + 1) * G.m + j);
     SVB_CHECK_LAUNCH();
+    k->normalized = j;
   });
 }
 
@@ -572,6 +857,7 @@ int svb_cg_restart(svb_krylov* k, void* stream) {
                                                   ptr<double>(k->p), ptr<double>(k->scal), ptr<double>(k->partials),
                                                   ptr<unsigned>(k->counter), k->st_dev);
     SVB_CHECK_LAUNCH();
+    mark(k, S(stream));
   });
 }
 
@@ -584,6 +870,7 @@ int svb_cg_step(svb_krylov* k, double bnorm, void* stream) {
                                      k->st_dev);
     k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
                                          ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev);
+    mark(k, s);  // status is final here; the p update overlaps the host
     k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal));
     note_launches(2);
     SVB_CHECK_LAUNCH();

@@ -32,42 +32,82 @@ constexpr int COO_TILE = COO_THREADS * COO_ITEMS;
 
 // ---------------------------------------------------------------------------
 // CSR/LibA/L — CSR-vector (kernels.py:167-189)
+//
+// Reference order: lane j%L of a row accumulates elements j, j+L, ...
+// sequentially from 0, then the halving tree lanes[:h] += lanes[h:2h].
+// A warp takes a tile of 32 rows and picks the effective lane count
+// Lp = min(L, next_pow2(longest row in the tile)).  This is exact: lanes
+// >= len only ever hold +0.0, so the tree steps h >= Lp each add +0.0 —
+// the first turns a -0.0 partial into +0.0, the rest are no-ops — and the
+// remaining steps are precisely the Lp-lane tree.  Short rows therefore get
+// 32/Lp rows per warp instead of one, and U row groups are interleaved so
+// every thread keeps U independent load chains in flight.
 // ---------------------------------------------------------------------------
 template <class T, class P, int L>
 __global__ void __launch_bounds__(256) k_csr_vector(int64_t nrows, const P* __restrict__ ptr,
                                                     const int* __restrict__ cols,
                                                     const T* __restrict__ vals,
                                                     const T* __restrict__ x, T* __restrict__ y) {
-  constexpr int G = 32 / L;  // rows per warp per step
+  constexpr int U = 4;
   const int lane = threadIdx.x & 31;
-  const int sub = lane & (L - 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp * G; base < nrows; base += nwarps * G) {  // warp-uniform
-    const int64_t row = base + lane / L;
-    int64_t s = 0, e = 0;
-    if (row < nrows) {
-      s = ptr[row];
-      e = ptr[row + 1];
+  for (int64_t t0 = warp * 32; t0 < nrows; t0 += nwarps * 32) {   // warp-uniform
+    const int64_t myrow = t0 + lane;
+    int64_t ms = 0, ml = 0;
+    if (myrow < nrows) {
+      ms = ptr[myrow];
+      ml = ptr[myrow + 1] - ms;
     }
-    T acc = T(0);
-    int64_t k = s + sub;
-    // two independent loads in flight per thread; accumulation stays in order
-    for (; k + L < e; k += 2 * L) {
-      const T v0 = ld_stream(vals + k), v1 = ld_stream(vals + k + L);
-      const int c0 = ld_stream(cols + k), c1 = ld_stream(cols + k + L);
-      const T p0 = v0 * ld_x(x + c0);
-      const T p1 = v1 * ld_x(x + c1);
-      acc = acc + p0;
-      acc = acc + p1;
-    }
-    if (k < e) acc = acc + ld_stream(vals + k) * ld_x(x + ld_stream(cols + k));
+    const unsigned longest = __reduce_max_sync(0xffffffffu, (unsigned)(ml < (1 << 30) ? ml : (1 << 30)));
+    int Lp = 1;
+    while (Lp < L && (unsigned)Lp < longest) Lp <<= 1;
+    const int G = 32 / Lp;          // rows per group
+    const int sub = lane & (Lp - 1);
+    const int slot = lane / Lp;
+    for (int g0 = 0; g0 < Lp; g0 += U) {   // Lp groups cover the 32-row tile
+      int64_t s[U], len[U];
+      T acc[U];
+      int64_t most = 0;
 #pragma unroll
-    for (int h = L / 2; h >= 1; h >>= 1) acc = acc + __shfl_down_sync(0xffffffffu, acc, h, L);
-    if (sub == 0 && row < nrows) y[row] = acc;
+      for (int u = 0; u < U; ++u) {
+        const int q = (g0 + u) * G + slot;           // row within the tile
+        const int src = q < 32 ? q : 0;
+        s[u] = __shfl_sync(0xffffffffu, ms, src);
+        len[u] = __shfl_sync(0xffffffffu, ml, src);
+        if (g0 + u >= Lp || q >= 32) len[u] = 0;
+        acc[u] = T(0);
+        most = len[u] > most ? len[u] : most;
+      }
+      for (int64_t t = sub; t < most; t += Lp) {
+        T v[U];
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t < len[u]) {
+            v[u] = ld_stream(vals + s[u] + t);
+            c[u] = ld_stream(cols + s[u] + t);
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t < len[u]) acc[u] = acc[u] + v[u] * ld_x(x + c[u]);
+      }
+      if (Lp < L) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = acc[u] + T(0);
+      }
+      for (int h = Lp >> 1; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = acc[u] + __shfl_down_sync(0xffffffffu, acc[u], h, Lp);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = (g0 + u) * G + slot;
+        if (sub == 0 && g0 + u < Lp && q < 32 && t0 + q < nrows) y[t0 + q] = acc[u];
+      }
+    }
   }
 }
-
 // ---------------------------------------------------------------------------
 // CSR/LibB (row-scalar, kernels.py:192-199) and CSR/LibC (merge-path chunks,
 // kernels.py:202-223): each CTA stages the products of its 128 rows into
