@@ -245,11 +245,53 @@ def algorithmic_bytes(tag: str, info, n: int) -> float:
     return 16 * nnz + 8 * ncols + 8 * n          # COO
 
 
-def mgs_bytes(n: int, j: int) -> float:
-    """One Arnoldi orthogonalisation at column j: dot0 reads V0,w (16n);
-    pass i=1..j reads w,V[i-1],V[i] and writes w (32n); final reads w,V[j],
-    writes w (24n)."""
-    return 16 * n + 32 * n * j + 24 * n
+def mgs_bytes(n: int, j: int, resident: bool = True) -> float:
+    """Algorithmic bytes of one Arnoldi orthogonalisation at column j.
+
+    Resident kernel (w kept on chip): read w once, each basis row V[0..j]
+    once, write the normalised w once -> 8n(j+3).  Streaming fallback: dot0
+    reads V0,w (16n); pass i reads w,V[i-1],V[i] and writes w (32n); final
+    reads w,V[j] and writes w (24n); normalise reads+writes w (16n)."""
+    if resident:
+        return 8 * n * (j + 3)
+    return 16 * n + 32 * n * j + 24 * n + 16 * n
+
+
+def config1_cg(P, device, _lib, models, start_cfg, reps: int = 3) -> dict:
+    """Side measurement (not `value`): BASELINE configs[0], CG fp64 on the 2-D
+    5-point Poisson 1024^2 (n = 1,048,576, nnz = 5,238,784), tol 1e-8,
+    b = A*1; async predict-while-solve from CSR/LibA/32 vs the fixed
+    default CSR-vector solve."""
+    import numpy as np
+    import torch
+    from paper_2411_10143_b200.solver import DeviceOptions
+    A = P.CsrMatrix.stencil((1024, 1024), [(0, 0), (0, -1), (0, 1), (-1, 0), (1, 0)],
+                            [4.0, -1.0, -1.0, -1.0, -1.0])
+    s = device.thread_stream()
+    ones = device.DeviceVector.from_numpy(np.ones(A.nrows), s)
+    b = device.DeviceVector(A.nrows)
+    _lib.check(_lib.lib().svb_spmv_sequential(A._device().handle, ones.ptr, b.ptr, s.handle))
+    s.sync()
+    params = P.GmresParams(tol=1e-8, max_iters=5000)
+    out = {"workload": "config1: CG fp64 Poisson 1024^2, tol 1e-8, b=A*1"}
+    with DeviceOptions(keep_solution_on_device=True):
+        P.async_solve(A, b, params, models, method="cg", initial_config=start_cfg)   # warm
+        ts, its, swaps = [], None, None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = P.async_solve(A, b, params, models, method="cg", initial_config=start_cfg)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+            its, swaps = r.iterations, [(x.iteration, x.config.token()) for x in r.config_timeline]
+        out.update({"async_s": statistics.median(ts), "iterations": its, "swaps": swaps,
+                    "converged": r.converged, "final_residual": r.final_residual})
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = P.cg_solve(A, b, params, initial_config=start_cfg)
+        torch.cuda.synchronize()
+        out.update({"default_csr_vector_s": time.perf_counter() - t0, "default_iterations": d.iterations})
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -371,7 +413,8 @@ def b200_arm(args):
             js = []
             for r in prof_reports:
                 js += [it % RESTART for it in range(r.iterations)]
-            byts = sum(mgs_bytes(n, j) for j in js[:len(ms)])
+            resident = os.environ.get("SPMVTUNE_MGS") != "stream"
+            byts = sum(mgs_bytes(n, j, resident) for j in js[:len(ms)])
         else:
             continue
         groups[tag] = {"launches": len(ms), "ms_total": tot, "ms_avg": tot / len(ms),
@@ -441,6 +484,8 @@ def b200_arm(args):
             torch.cuda.synchronize()
             detail["sequential_gpu_s"] = time.perf_counter() - t0
             detail["sequential_phases"] = sq.phases
+        if not args.no_extra:
+            detail["config1_cg"] = config1_cg(P, device, _lib, models, start_cfg)
     detail.update({
         "iterations": last.iterations, "converged": last.converged,
         "final_residual": last.final_residual,
@@ -483,6 +528,7 @@ def main(argv=None):
     ap.add_argument("--total-iters", type=int, default=77,
                     help="reference arm: GMRES iterations the solve takes (77 at config 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-1 CG side measurement")
     args = ap.parse_args(argv)
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("--steps >= 1 and --warmup >= 0")

@@ -107,6 +107,8 @@ int svb_host_free(void* ptr);
 int svb_copy(void* dst, const void* src, int64_t bytes, void* stream);  /* any direction, async */
 int svb_memset(void* dst, int value, int64_t bytes, void* stream);
 int svb_device_info(int32_t* sm_count, int64_t* free_bytes, int64_t* total_bytes);
+/* stream-ordered pool: bytes reserved from the driver / currently in use */
+int svb_pool_info(int64_t* reserved_bytes, int64_t* used_bytes);
 
 /* ---- containers (formats.py:50-260) ------------------------------------ */
 /* CooMatrix(nrows, ncols, rows, cols, values): row-major sorted, no dups. */
@@ -179,7 +181,8 @@ typedef struct {
   double hjj;        /* rotated H[j,j] (GMRES breakdown check) */
   double pq;         /* p.Ap (CG) */
   int32_t nonfinite; /* a non-finite scalar was produced */
-  int32_t pad;
+  int32_t done;      /* batched CG: 0 running, 1 tol met, 2 p.Ap == 0, 3 non-finite */
+  int64_t count;     /* batched CG: iterations executed since svb_cg_batch_reset */
 } svb_krylov_status;
 
 /* n rows, restart m (GMRES; m = 0 for CG).  Owns V[(m+1) x n], H, Givens
@@ -209,6 +212,15 @@ int svb_cg_restart(svb_krylov* k, void* stream);
 /* CG after q = A p: alpha = rr/(p.q); x += alpha p; r -= alpha q; rr' = r.r;
  * estimate = sqrt(rr')/bnorm; p = r + (rr'/rr) p */
 int svb_cg_step(svb_krylov* k, double bnorm, void* stream);
+
+/* Batched CG: the host enqueues many iterations (SpMV + svb_cg_step_batched)
+ * without reading status in between; once an iteration meets `tol` (or hits
+ * p.Ap == 0 / a non-finite value) the remaining kernels of the batch are
+ * no-ops, so x and r stay at that iteration.  Estimates are logged on device. */
+int svb_cg_batch_reset(svb_krylov* k, double tol, int64_t history_cap, void* stream);
+int svb_cg_batch_resume(svb_krylov* k, void* stream);   /* clear `done`, keep count */
+int svb_cg_step_batched(svb_krylov* k, double bnorm, void* stream);
+int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, void* stream);
 
 /* ---- generic fused vector ops (device vectors of length n) -------------- */
 int svb_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host,

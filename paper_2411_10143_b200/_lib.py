@@ -41,7 +41,7 @@ class MatrixInfo(C.Structure):
 class KrylovStatus(C.Structure):
     _fields_ = [("beta", C.c_double), ("hnext", C.c_double), ("estimate", C.c_double),
                 ("hjj", C.c_double), ("pq", C.c_double), ("nonfinite", C.c_int32),
-                ("pad", C.c_int32)]
+                ("done", C.c_int32), ("count", C.c_int64)]
 
 
 # name -> argtypes (all functions return int status unless listed in _RESTYPE)
@@ -64,6 +64,7 @@ _SIGS = {
     "svb_copy": [_P, _P, _I64, _P],
     "svb_memset": [_P, C.c_int, _I64, _P],
     "svb_device_info": [C.POINTER(C.c_int32), _PI64, _PI64],
+    "svb_pool_info": [_PI64, _PI64],
     "svb_coo_create": [_I64, _I64, _I64, _P, _P, _P, _P, _PP],
     "svb_csr_create": [_I64, _I64, _I64, _P, _P, _P, _P, _PP],
     "svb_ell_create": [_I64, _I64, _I64, _P, _P, _P, _PP],
@@ -91,6 +92,10 @@ _SIGS = {
     "svb_gmres_update_x": [_P, _I32, _P],
     "svb_cg_restart": [_P, _P],
     "svb_cg_step": [_P, _D, _P],
+    "svb_cg_batch_reset": [_P, _D, _I64, _P],
+    "svb_cg_batch_resume": [_P, _P],
+    "svb_cg_step_batched": [_P, _D, _P],
+    "svb_cg_history": [_P, _I64, _I64, _PD, _P],
     "svb_dot": [_P, _P, _I64, _PD, _P],
     "svb_forest_create": [_I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _PP],
     "svb_forest_destroy": [_P],

@@ -36,6 +36,8 @@ struct svb_krylov {
   // this, not on the stream, so work enqueued behind it (the speculative
   // next SpMV, CG's p update) overlaps the host's decision
   cudaEvent_t ev = nullptr;
+  svb::Buf ctl, hist;   // batched-CG control block and estimate log
+  int64_t hist_cap = 0;
   ~svb_krylov() {
     if (ev) cudaEventDestroy(ev);
     if (st_host) cudaFreeHost(st_host);
@@ -418,17 +420,30 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_resident(Gm G, int j, double b
   const int len = hi > lo ? (int)(hi - lo) : 0;
   double* wg = G.V + (int64_t)(j + 1) * G.ld + lo;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  auto row = [&](int i) { return G.V + (int64_t)i * G.ld + lo; };
 
-  // Loads are issued in batches of U per thread before any shared-memory
-  // update, so U independent 8-byte loads per operand stay in flight (the
-  // basis rows are read-only here: V[j+1] is written only after the last
-  // read).  Elements k = tid + u*PB keep every warp access coalesced.
+  // Element k of this CTA's slice is handled by thread k % PB; batches of U
+  // elements per thread keep 2U independent loads in flight.  The first
+  // batch of the NEXT pass is loaded into registers before each grid
+  // barrier, so the barrier's latency overlaps those loads; the rest of the
+  // next pass's rows are pulled into L2 by a bulk prefetch.  The basis rows
+  // are read-only here (V[j+1] is written only after the last read).
   constexpr int U = 8;
+  double pa[U], pb[U];   // preloaded first batch of the coming pass
+  auto preload = [&](const double* a, const double* b) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = threadIdx.x + u * PB;
+      pa[u] = k < len ? __ldcs(a + k) : 0.0;
+      pb[u] = (b != nullptr && k < len) ? __ldcg(b + k) : 0.0;
+    }
+  };
+
   // pass 0: stage w, h_0 = V_0 . w
   double acc = 0.0;
-  if (j >= 1) prefetch_slice_l2(G.V + G.ld + lo, len);
+  if (j >= 1) prefetch_slice_l2(row(1), len);
   {
-    const double* v0 = G.V + lo;
+    const double* v0 = row(0);
     for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
       double a[U], b[U];
 #pragma unroll
@@ -445,15 +460,26 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_resident(Gm G, int j, double b
       }
     }
   }
+  preload(row(0), j >= 1 ? row(1) : nullptr);
   double h = fused_grid_sum(acc, gparts, gcounter, 0, scratch);
   if (lead) G.H[j] = h;
+
   // passes 1..j: w -= h_{i-1} V_{i-1};  h_i = V_i . w
   for (int i = 1; i <= j; ++i) {
-    const double* vp = G.V + (int64_t)(i - 1) * G.ld + lo;
-    const double* vi = G.V + (int64_t)i * G.ld + lo;
-    if (i + 1 <= j) prefetch_slice_l2(G.V + (int64_t)(i + 1) * G.ld + lo, len);
+    const double* vp = row(i - 1);
+    const double* vi = row(i);
+    if (i + 1 <= j) prefetch_slice_l2(row(i + 1), len);
     acc = 0.0;
-    for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {   // preloaded first batch
+      const int k = threadIdx.x + u * PB;
+      if (k < len) {
+        const double w = ws[k] - h * pa[u];
+        ws[k] = w;
+        acc += pb[u] * w;
+      }
+    }
+    for (int k0 = threadIdx.x + U * PB; k0 < len; k0 += U * PB) {
       double a[U], b[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -471,14 +497,25 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_resident(Gm G, int j, double b
         }
       }
     }
+    preload(vi, i + 1 <= j ? row(i + 1) : nullptr);
     h = fused_grid_sum(acc, gparts, gcounter, i, scratch);
     if (lead) G.H[i * G.m + j] = h;
   }
+
   // final: w -= h_j V_j; hnext = ||w||; V[j+1] = w / hnext
+  acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int k = threadIdx.x + u * PB;
+    if (k < len) {
+      const double w = ws[k] - h * pa[u];
+      ws[k] = w;
+      acc += w * w;
+    }
+  }
   {
-    const double* vj = G.V + (int64_t)j * G.ld + lo;
-    acc = 0.0;
-    for (int k0 = threadIdx.x; k0 < len; k0 += U * PB) {
+    const double* vj = row(j);
+    for (int k0 = threadIdx.x + U * PB; k0 < len; k0 += U * PB) {
       double a[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -570,10 +607,24 @@ __global__ void __launch_bounds__(KB) k_cg_restart(int64_t n, const double* __re
   }
 }
 
+// Batched-CG control block (device memory): kernels of a batch become no-ops
+// once `done` is set, so the host can enqueue many iterations and read the
+// status once per batch; the estimate of every executed iteration is logged.
+struct CgCtl {
+  int done;       // CG_* reason, 0 while running
+  int count;      // iterations executed since the last reset
+  int cap;        // history capacity
+  int pad;
+  double tol;
+  double* hist;   // per-iteration residual estimates
+};
+enum { CG_RUN = 0, CG_TOL = 1, CG_PQ0 = 2, CG_NONFINITE = 3 };
+
 // alpha = rr / (p.q)
 __global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restrict__ p,
                                               const double* __restrict__ q, double* scal, double* partials,
-                                              unsigned* counter, svb_krylov_status* st) {
+                                              unsigned* counter, svb_krylov_status* st, CgCtl* ctl) {
+  if (ctl != nullptr && ctl->done) return;
   double acc = 0.0;
   for_pairs(
       n,
@@ -588,6 +639,10 @@ __global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restric
     st->pq = tot;
     st->nonfinite = bad(tot);
     scal[S_ALPHA] = tot != 0.0 ? scal[S_RR] / tot : 0.0;
+    if (ctl != nullptr && (bad(tot) || tot == 0.0)) {
+      ctl->done = bad(tot) ? CG_NONFINITE : CG_PQ0;
+      st->done = ctl->done;
+    }
   }
 }
 
@@ -595,7 +650,8 @@ __global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restric
 __global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
                                                   const double* __restrict__ p, const double* __restrict__ q,
                                                   double* scal, double bnorm, double* partials,
-                                                  unsigned* counter, svb_krylov_status* st) {
+                                                  unsigned* counter, svb_krylov_status* st, CgCtl* ctl) {
+  if (ctl != nullptr && ctl->done) return;
   const double alpha = scal[S_ALPHA];
   double acc = 0.0;
   for_pairs(
@@ -622,14 +678,24 @@ __global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict_
     const double rr_old = scal[S_RR];
     scal[S_BETA] = tot / rr_old;
     scal[S_RR] = tot;
-    st->estimate = sqrt(tot) / bnorm;
-    st->nonfinite = st->nonfinite || bad(tot) || bad(st->estimate);
+    const double est = sqrt(tot) / bnorm;
+    st->estimate = est;
+    st->nonfinite = st->nonfinite || bad(tot) || bad(est);
+    if (ctl != nullptr) {
+      if (ctl->count < ctl->cap) ctl->hist[ctl->count] = est;
+      ctl->count += 1;
+      st->count = ctl->count;
+      if (bad(tot) || bad(est)) ctl->done = CG_NONFINITE;
+      else if (est <= ctl->tol) ctl->done = CG_TOL;
+      st->done = ctl->done;
+    }
   }
 }
 
 // p = r + beta p
 __global__ void __launch_bounds__(KB) k_cg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
-                                             const double* scal) {
+                                             const double* scal, const CgCtl* ctl) {
+  if (ctl != nullptr && ctl->done) return;
   const double beta = scal[S_BETA];
   for_pairs(
       n,
@@ -867,13 +933,71 @@ int svb_cg_step(svb_krylov* k, double bnorm, void* stream) {
     double* P = ptr<double>(k->partials);
     unsigned* C = ptr<unsigned>(k->counter);
     k_cg_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->scal), P, C,
-                                     k->st_dev);
+                                     k->st_dev, nullptr);
     k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
-                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev);
+                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev, nullptr);
     mark(k, s);  // status is final here; the p update overlaps the host
-    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal));
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal), nullptr);
     note_launches(2);
     SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_cg_batch_reset(svb_krylov* k, double tol, int64_t cap, void* stream) {
+  return guard([&] {
+    cudaStream_t s = S(stream);
+    if (cap < 1) cap = 1;
+    if (!k->hist || k->hist_cap < cap) {
+      k->hist = alloc(cap * sizeof(double), s);
+      detach(k->hist);
+      k->hist_cap = cap;
+    }
+    if (!k->ctl) {
+      k->ctl = alloc(sizeof(CgCtl), s);
+      detach(k->ctl);
+    }
+    CgCtl c{CG_RUN, 0, (int)std::min<int64_t>(k->hist_cap, INT32_MAX), 0, tol, ptr<double>(k->hist)};
+    SVB_CUDA_TRY(cudaMemcpyAsync(k->ctl->ptr, &c, sizeof(c), cudaMemcpyHostToDevice, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));   // `c` is a host temporary
+    k->st_host->done = 0;
+    k->st_host->count = 0;
+  });
+}
+
+int svb_cg_batch_resume(svb_krylov* k, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k->ctl, SVB_INVALID, "svb_cg_batch_reset first");
+    SVB_CUDA_TRY(cudaMemsetAsync(k->ctl->ptr, 0, sizeof(int), S(stream)));   // done = 0
+    SVB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    k->st_host->done = 0;
+  });
+}
+
+int svb_cg_step_batched(svb_krylov* k, double bnorm, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k->ctl, SVB_INVALID, "svb_cg_batch_reset first");
+    cudaStream_t s = S(stream);
+    double* P = ptr<double>(k->partials);
+    unsigned* C = ptr<unsigned>(k->counter);
+    CgCtl* ctl = ptr<CgCtl>(k->ctl);
+    k_cg_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->scal), P, C,
+                                     k->st_dev, ctl);
+    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
+                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev, ctl);
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal), ctl);
+    note_launches(2);
+    SVB_CHECK_LAUNCH();
+    mark(k, s);
+  });
+}
+
+int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k->hist && first >= 0 && first + count <= k->hist_cap, SVB_INVALID, "history range");
+    if (count <= 0) return;
+    SVB_CUDA_TRY(cudaMemcpyAsync(host, ptr<double>(k->hist) + first, count * sizeof(double),
+                                 cudaMemcpyDeviceToHost, S(stream)));
+    SVB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
   });
 }
 

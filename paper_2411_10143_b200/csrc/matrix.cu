@@ -297,6 +297,20 @@ int svb_memset(void* dst, int value, int64_t bytes, void* stream) {
     if (bytes > 0) SVB_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, S(stream)));
   });
 }
+int svb_pool_info(int64_t* reserved, int64_t* used) {
+  return guard([&] {
+    int dev = 0;
+    SVB_CUDA_TRY(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    SVB_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t r = 0, u = 0;
+    SVB_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    SVB_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    *reserved = (int64_t)r;
+    *used = (int64_t)u;
+  });
+}
+
 int svb_device_info(int32_t* sms, int64_t* free_b, int64_t* total_b) {
   return guard([&] {
     size_t f = 0, t = 0;

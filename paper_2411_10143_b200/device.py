@@ -78,6 +78,22 @@ def thread_stream(priority: int = 0) -> Stream:
     return s
 
 
+_shared = {}
+_shared_lock = threading.Lock()
+
+
+def shared_stream(priority: int) -> Stream:
+    """A process-wide stream (created once): advisor threads are short-lived,
+    and creating/destroying a CUDA stream per solve costs milliseconds."""
+    s = _shared.get(priority)
+    if s is None:
+        with _shared_lock:
+            s = _shared.get(priority)
+            if s is None:
+                s = _shared[priority] = Stream(priority)
+    return s
+
+
 class DeviceVector:
     """A device buffer of ``n`` elements (float64 by default)."""
 
@@ -140,4 +156,7 @@ def device_info() -> dict:
     free = ctypes.c_int64()
     total = ctypes.c_int64()
     _lib.check(_lib.lib().svb_device_info(ctypes.byref(sms), ctypes.byref(free), ctypes.byref(total)))
-    return {"sm_count": sms.value, "free_bytes": free.value, "total_bytes": total.value}
+    res, used = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().svb_pool_info(ctypes.byref(res), ctypes.byref(used)))
+    return {"sm_count": sms.value, "free_bytes": free.value, "total_bytes": total.value,
+            "pool_reserved_bytes": res.value, "pool_used_bytes": used.value}

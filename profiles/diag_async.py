@@ -42,6 +42,25 @@ def timed_pipeline(self, cancel):
 
 
 solver._Advisor._pipeline = timed_pipeline
+if len(sys.argv) > 2 and sys.argv[2] == "nvml":
+    import threading
+    import pynvml
+    pynvml.nvmlInit()
+    hdl = pynvml.nvmlDeviceGetHandleByIndex(0)
+    what = sys.argv[3] if len(sys.argv) > 3 else "all"
+
+    def sampler():
+        while True:
+            pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM)
+            if what == "all":
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+                pynvml.nvmlDeviceGetUtilizationRates(hdl)
+            time.sleep(0.05)
+    threading.Thread(target=sampler, daemon=True).start()
+if "nogc" in sys.argv:
+    import gc
+    gc.collect()
+    gc.disable()
 out = []
 for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 8):
     stamps = []
@@ -57,5 +76,8 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 8):
     gaps = [round((first[its[k]] - first[its[k - 1]]) * 1e3, 2) for k in range(1, min(len(its), 12))]
     out.append({"wall_ms": round(wall * 1e3, 1), "swaps": [(x.iteration, x.config.token(),
                 round(x.swap_cost_seconds * 1e3, 2)) for x in r.config_timeline],
-                "first_iter_gaps_ms": gaps, "iters": r.iterations})
+                "first_iter_gaps_ms": gaps, "iters": r.iterations,
+                "free_gb": round(device.device_info()["free_bytes"] / 1e9, 2),
+                "pool_gb": [round(device.device_info()[k] / 1e9, 2)
+                            for k in ("pool_reserved_bytes", "pool_used_bytes")]})
     print(json.dumps(out[-1]), flush=True)
