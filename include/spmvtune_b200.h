@@ -226,6 +226,25 @@ int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, vo
 int svb_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host,
             void* stream);
 
+/* Building blocks of the row-partitioned (multi-GPU) solvers: every
+ * reduction writes its LOCAL result to a device scalar, which the caller
+ * all-reduces in place (NCCL) before the next primitive reads it — scalars
+ * never visit the host inside a step.  Deterministic fixed-order sums. */
+typedef struct svb_vecops svb_vecops;
+int svb_vecops_create(int64_t n, svb_vecops** out);
+int svb_vecops_destroy(svb_vecops* v);
+/* *out_dev = x . y */
+int svb_vec_dot(svb_vecops* v, const double* x_dev, const double* y_dev, double* out_dev,
+                void* stream);
+/* y += sign * (*alpha_dev) * x;  *out_dev = (z ? z : y) . y   (out_dev may be NULL) */
+int svb_vec_axpy_dot(svb_vecops* v, const double* alpha_dev, double sign, const double* x_dev,
+                     double* y_dev, const double* z_dev, double* out_dev, void* stream);
+/* y = a x + b y */
+int svb_vec_axpby(svb_vecops* v, double a, const double* x_dev, double b, double* y_dev,
+                  void* stream);
+/* x *= s */
+int svb_vec_scale(svb_vecops* v, double* x_dev, double s, void* stream);
+
 /* ---- compiled cascade inference (inference.py:55-125, model_schema.md) ---
  * Flattened tree ensemble: node arrays in the reference's flattening order;
  * leaves carry feature = -1.  Evaluation: `<=` goes left, per-class sums in

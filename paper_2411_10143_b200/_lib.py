@@ -97,6 +97,12 @@ _SIGS = {
     "svb_cg_step_batched": [_P, _D, _P],
     "svb_cg_history": [_P, _I64, _I64, _PD, _P],
     "svb_dot": [_P, _P, _I64, _PD, _P],
+    "svb_vecops_create": [_I64, _PP],
+    "svb_vecops_destroy": [_P],
+    "svb_vec_dot": [_P, _P, _P, _P, _P],
+    "svb_vec_axpy_dot": [_P, _P, _D, _P, _P, _P, _P, _P],
+    "svb_vec_axpby": [_P, _D, _P, _D, _P, _P],
+    "svb_vec_scale": [_P, _P, _D, _P],
     "svb_forest_create": [_I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _PP],
     "svb_forest_destroy": [_P],
     "svb_forest_predict": [_P, _P, _P, _P],

@@ -44,6 +44,12 @@ struct svb_krylov {
   }
 };
 
+struct svb_vecops {
+  int64_t n = 0;
+  unsigned grid = 1;
+  svb::Buf partials;  // grid doubles + reduction counter
+};
+
 namespace svb {
 
 constexpr int KB = 256;  // threads per CTA for the Krylov kernels
@@ -706,6 +712,36 @@ __global__ void __launch_bounds__(KB) k_cg_p(int64_t n, const double* __restrict
       [&](int64_t e) { p[e] = r[e] + beta * p[e]; });
 }
 
+// ---------------------------------------------------------------------------
+// building blocks for the row-partitioned solvers (device-scalar results)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(KB) k_axpy_dot(int64_t n, const double* __restrict__ alpha, double sign,
+                                                 const double* __restrict__ x, double* __restrict__ y,
+                                                 const double* __restrict__ z, double* partials,
+                                                 unsigned* counter, double* out) {
+  const double a = sign * (*alpha);
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double yy = y[e] + a * x[e];
+    y[e] = yy;
+    acc += (z ? z[e] : yy) * yy;
+  }
+  if (out == nullptr) return;
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = tot;
+}
+
+__global__ void __launch_bounds__(KB) k_axpby(int64_t n, double a, const double* __restrict__ x, double b,
+                                              double* __restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = a * x[e] + b * y[e];
+}
+
+__global__ void __launch_bounds__(KB) k_vscale(int64_t n, double* __restrict__ x, double s) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    x[e] *= s;
+}
+
 // generic dot for the host API
 __global__ void __launch_bounds__(KB) k_dot(int64_t n, const double* __restrict__ a,
                                             const double* __restrict__ b, double* partials,
@@ -998,6 +1034,60 @@ int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, vo
     SVB_CUDA_TRY(cudaMemcpyAsync(host, ptr<double>(k->hist) + first, count * sizeof(double),
                                  cudaMemcpyDeviceToHost, S(stream)));
     SVB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int svb_vecops_create(int64_t n, svb_vecops** out) {
+  return guard([&] {
+    auto v = new svb_vecops();
+    v->n = n;
+    v->grid = grid_for(n, KB, 4);
+    v->partials = alloc(v->grid * 8 + 64, 0);
+    detach(v->partials);
+    SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(v->partials->ptr) + v->grid * 8, 0, 64, 0));
+    SVB_CUDA_TRY(cudaStreamSynchronize(0));
+    *out = v;
+  });
+}
+
+int svb_vecops_destroy(svb_vecops* v) {
+  return guard([&] {
+    SVB_CUDA_TRY(cudaDeviceSynchronize());
+    delete v;
+  });
+}
+
+static unsigned* vctr(svb_vecops* v) {
+  return reinterpret_cast<unsigned*>(static_cast<char*>(v->partials->ptr) + v->grid * 8);
+}
+
+int svb_vec_dot(svb_vecops* v, const double* x, const double* y, double* out, void* stream) {
+  return guard([&] {
+    k_dot<<<v->grid, KB, 0, S(stream)>>>(v->n, x, y, ptr<double>(v->partials), vctr(v), out);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_vec_axpy_dot(svb_vecops* v, const double* alpha, double sign, const double* x, double* y,
+                     const double* z, double* out, void* stream) {
+  return guard([&] {
+    k_axpy_dot<<<v->grid, KB, 0, S(stream)>>>(v->n, alpha, sign, x, y, z, ptr<double>(v->partials), vctr(v),
+                                               out);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_vec_axpby(svb_vecops* v, double a, const double* x, double b, double* y, void* stream) {
+  return guard([&] {
+    k_axpby<<<v->grid, KB, 0, S(stream)>>>(v->n, a, x, b, y);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_vec_scale(svb_vecops* v, double* x, double s, void* stream) {
+  return guard([&] {
+    k_vscale<<<v->grid, KB, 0, S(stream)>>>(v->n, x, s);
+    SVB_CHECK_LAUNCH();
   });
 }
 

@@ -1,0 +1,515 @@
+"""Row-partitioned CG / GMRES across GPUs.
+
+One process per GPU (torchrun), NCCL over NVLink/NVSwitch for the exchange:
+
+* rows are split into contiguous blocks balanced by nnz (``partition_rows``);
+* every rank stores its block as a local CSR whose columns index a *window*
+  ``[cmin, cmax]`` of the global vector; the window is filled before each
+  SpMV by a halo exchange (``HaloPlan``: each peer sends exactly the slice of
+  its own rows that falls in my window — the neighbouring planes for a
+  stencil, wider ranges for irregular matrices);
+* dot products are computed locally into DEVICE scalars and summed in place
+  with an all-reduce, so scalars never leave the GPU inside a step; the host
+  reads one small block per iteration (GMRES: the Hessenberg column and
+  ||w||^2, after which the Givens update runs on the host exactly as the
+  reference's _gmres_core does; CG: p.Ap and r.r);
+* the cascade runs on GLOBAL features: the seven integer aggregates are
+  all-reduced (sum / max / min) and the diagonal count is the union of the
+  ranks' diagonal-offset sets, so the predicted configuration equals the
+  single-GPU prediction bit for bit.
+
+The driver is written against two small interfaces — ``ops`` (local vector
+kernels) and ``comm`` (collectives) — so the same control flow runs with
+``CudaOps``/``NcclComm`` in production and with numpy/gloo doubles in the
+CPU test suite (tests/test_distributed.py).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, device
+from .errors import SolverNumericalError, StagnationError
+from .features import FeatureVector, device_aggregates, features_from_aggregates
+from .formats import CsrMatrix, FormatTag, convert
+from .kernels import Library, SpmvConfig, default_workers, launch
+
+__all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
+           "NcclComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve"]
+
+
+# ---------------------------------------------------------------------------
+# partition and halo plan (pure host logic)
+# ---------------------------------------------------------------------------
+def partition_rows(row_ptr: np.ndarray, world: int) -> np.ndarray:
+    """Contiguous row bounds [0 = b0 <= ... <= b_world = n] balancing nnz."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n, nnz = row_ptr.size - 1, int(row_ptr[-1])
+    if nnz == 0:
+        return np.linspace(0, n, world + 1).astype(np.int64)
+    targets = (np.arange(world + 1, dtype=np.float64) * nnz / world)
+    b = np.searchsorted(row_ptr, targets, side="left").astype(np.int64)
+    b[0], b[-1] = 0, n
+    return np.maximum.accumulate(np.minimum(b, n))
+
+
+@dataclass
+class LocalBlock:
+    """Rank-local CSR rows [r0, r1) with columns relative to the window."""
+
+    r0: int
+    r1: int
+    cmin: int
+    cmax: int
+    row_ptr: np.ndarray
+    cols: np.ndarray          # window-relative
+    values: np.ndarray
+    ncols_global: int
+    offsets: np.ndarray       # distinct global diagonal offsets (col - row) of the block
+
+    @property
+    def nloc(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def window(self) -> int:
+        return self.cmax - self.cmin + 1
+
+
+def local_block(row_ptr, col_idx, values, r0: int, r1: int, ncols: int) -> LocalBlock:
+    """Slice rows [r0, r1) of a global host CSR into a windowed local block.
+    The window always covers the rank's own rows so the local slice of x
+    lives inside it."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    s, e = int(row_ptr[r0]), int(row_ptr[r1])
+    cols = np.asarray(col_idx[s:e], dtype=np.int64)
+    cmin = min(int(cols.min()) if cols.size else r0, r0)
+    cmax = max(int(cols.max()) if cols.size else r1 - 1, r1 - 1)
+    lp = row_ptr[r0:r1 + 1] - s
+    rows = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(lp))
+    offs = np.unique(cols - rows)
+    return LocalBlock(r0, r1, cmin, cmax, lp, cols - cmin, np.asarray(values[s:e], np.float64),
+                      int(ncols), offs)
+
+
+@dataclass
+class HaloPlan:
+    """Who sends which global range to whom.  ``recvs``/``sends`` hold
+    (peer, lo, hi) global index ranges; a rank receives the part of its
+    window owned by each peer and sends the part of its rows in each peer's
+    window."""
+
+    rank: int
+    recvs: list
+    sends: list
+
+    @classmethod
+    def build(cls, bounds, windows, rank: int) -> "HaloPlan":
+        world = len(bounds) - 1
+        cmin, cmax = windows[rank]
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        recvs, sends = [], []
+        for j in range(world):
+            if j == rank:
+                continue
+            lo, hi = max(cmin, int(bounds[j])), min(cmax + 1, int(bounds[j + 1]))
+            if lo < hi:
+                recvs.append((j, lo, hi))
+            pmin, pmax = windows[j]
+            lo, hi = max(pmin, r0), min(pmax + 1, r1)
+            if lo < hi:
+                sends.append((j, lo, hi))
+        return cls(rank, recvs, sends)
+
+    def bytes_per_exchange(self) -> int:
+        return 8 * sum(hi - lo for _, lo, hi in self.recvs)
+
+
+# ---------------------------------------------------------------------------
+# device implementations of the two interfaces
+# ---------------------------------------------------------------------------
+class _DevView:
+    """(pointer, count) view of float64 device memory, exportable to NCCL."""
+
+    __slots__ = ("ptr", "n")
+
+    def __init__(self, ptr: int, n: int):
+        self.ptr, self.n = int(ptr), int(n)
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, False), "version": 3,
+                "strides": None}
+
+
+class CudaOps:
+    """Local vector kernels on this rank's GPU (C ABI svb_vec_*)."""
+
+    def __init__(self, n_loc: int, stream: device.Stream):
+        self.n = int(n_loc)
+        self.stream = stream
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().svb_vecops_create(self.n, ctypes.byref(h)))
+        self.h = h.value
+        self.L = _lib.lib()
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            try:
+                _lib.load().svb_vecops_destroy(h)
+            except Exception:
+                pass
+
+    # storage
+    def vec(self, n: int | None = None) -> device.DeviceVector:
+        v = device.DeviceVector(self.n if n is None else n)
+        device.memset(v.ptr, 0, v.nbytes, self.stream)
+        return v
+
+    def scalars(self, k: int) -> device.DeviceVector:
+        return self.vec(k)
+
+    def view(self, v, offset: int, count: int) -> _DevView:
+        return _DevView(v.ptr + 8 * offset, count)
+
+    def upload(self, v, a: np.ndarray):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        device.copy(v.ptr, a.ctypes.data, a.nbytes, self.stream)
+        self.stream.sync()
+
+    def fetch(self, v) -> np.ndarray:
+        return v.to_numpy(self.stream)
+
+    def read(self, sc, count: int) -> np.ndarray:
+        out = np.empty(count)
+        device.copy(out.ctypes.data, sc.ptr, 8 * count, self.stream)
+        self.stream.sync()
+        return out
+
+    def copy(self, dst_view: _DevView, src_view: _DevView):
+        device.copy(dst_view.ptr, src_view.ptr, 8 * src_view.n, self.stream)
+
+    # kernels
+    def dot(self, x, y, sc, i: int):
+        _lib.check(self.L.svb_vec_dot(self.h, x.ptr, y.ptr, sc.ptr + 8 * i, self.stream.handle))
+
+    def axpy_dot(self, sc_a, ia: int, sign: float, x, y, z, sc_out, io: int | None):
+        _lib.check(self.L.svb_vec_axpy_dot(self.h, sc_a.ptr + 8 * ia, sign, x.ptr, y.ptr,
+                                           z.ptr if z is not None else None,
+                                           (sc_out.ptr + 8 * io) if sc_out is not None else None,
+                                           self.stream.handle))
+
+    def axpby(self, a: float, x, b: float, y):
+        _lib.check(self.L.svb_vec_axpby(self.h, a, x.ptr, b, y.ptr, self.stream.handle))
+
+    def scale(self, x, s: float):
+        _lib.check(self.L.svb_vec_scale(self.h, x.ptr, s, self.stream.handle))
+
+    def spmv(self, mat, cfg: SpmvConfig, window, dst):
+        launch(cfg, mat, window.ptr, dst.ptr, workers=default_workers(), stream=self.stream)
+
+    def local_csr(self, block: LocalBlock) -> CsrMatrix:
+        m = getattr(block, "_dev_csr", None)
+        if m is None:
+            m = CsrMatrix(block.nloc, block.window, block.row_ptr, block.cols, block.values)
+            block._dev_csr = m
+        return m
+
+    def prepare(self, block: LocalBlock, cfg: SpmvConfig):
+        csr = self.local_csr(block)
+        return csr if cfg.format is FormatTag.CSR else convert(csr, cfg.format)
+
+
+class NcclComm:
+    """torch.distributed (NCCL) collectives ordered on the solver stream."""
+
+    def __init__(self, stream: device.Stream):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.ext = torch.cuda.ExternalStream(stream.handle)
+
+    def _t(self, v):
+        return self.torch.as_tensor(v if isinstance(v, _DevView) else _DevView(v.ptr, v.n),
+                                    device="cuda")
+
+    def allreduce(self, sc, first: int, count: int):
+        with self.torch.cuda.stream(self.ext):
+            self.dist.all_reduce(self._t(_DevView(sc.ptr + 8 * first, count)))
+
+    def allreduce_max(self, arr: np.ndarray) -> np.ndarray:
+        t = self.torch.as_tensor(arr, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    def allgather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def exchange(self, sends, recvs):
+        ops = [self.dist.P2POp(self.dist.isend, self._t(v), peer) for peer, v in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, self._t(v), peer) for peer, v in recvs]
+        if not ops:
+            return
+        with self.torch.cuda.stream(self.ext):
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+# ---------------------------------------------------------------------------
+# distributed operator: halo exchange + local SpMV
+# ---------------------------------------------------------------------------
+class DistOperator:
+    def __init__(self, block: LocalBlock, bounds, comm, ops, cfg: SpmvConfig):
+        self.block, self.comm, self.ops, self.cfg = block, comm, ops, cfg
+        windows = comm.allgather_obj((block.cmin, block.cmax))
+        self.plan = HaloPlan.build(bounds, windows, comm.rank)
+        self.window = ops.vec(block.window)
+        self.own = block.r0 - block.cmin
+        self.mat = ops.prepare(block, cfg)
+
+    def swap(self, cfg: SpmvConfig):
+        self.cfg = cfg
+        self.mat = self.ops.prepare(self.block, cfg)
+
+    def apply(self, src, dst):
+        """dst = A_local * x, with x's local slice in ``src``."""
+        b, ops = self.block, self.ops
+        ops.copy(ops.view(self.window, self.own, b.nloc), ops.view(src, 0, b.nloc))
+        sends = [(p, ops.view(src, lo - b.r0, hi - lo)) for p, lo, hi in self.plan.sends]
+        recvs = [(p, ops.view(self.window, lo - b.cmin, hi - lo)) for p, lo, hi in self.plan.recvs]
+        self.comm.exchange(sends, recvs)
+        ops.spmv(self.mat, self.cfg, self.window, dst)
+
+
+# ---------------------------------------------------------------------------
+# solvers (control flow = reference _gmres_core / oracle cg)
+# ---------------------------------------------------------------------------
+def _finite(v: float, what: str, it: int):
+    if not math.isfinite(v):
+        raise SolverNumericalError(f"non-finite {what} at iteration {it}; aborting")
+
+
+def _global_norm2(ops, comm, x, sc, slot: int) -> float:
+    ops.dot(x, x, sc, slot)
+    comm.allreduce(sc, slot, 1)
+    return float(ops.read(sc, slot + 1)[slot])
+
+
+def dist_gmres(A: DistOperator, b_local, params) -> dict:
+    """Restarted MGS-GMRES over row-partitioned vectors.  Per Arnoldi step:
+    one halo exchange + local SpMV, j+2 fused local passes each followed by
+    an in-place all-reduce of one device scalar, one host read of the
+    column; Givens on the host (solver.py:294-313)."""
+    ops, comm = A.ops, A.comm
+    m = params.restart_m
+    V = [ops.vec() for _ in range(m + 1)]
+    x, tmp, bvec = ops.vec(), ops.vec(), ops.vec()
+    ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
+        ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
+    H = ops.scalars(m + 2)            # column buffer: h_0..h_j, ||w||^2
+    sc = ops.scalars(4)
+    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 0))
+    hist, done = [], 0
+    Hh = np.zeros((m + 1, m))
+
+    def out(conv, fin, status="ok"):
+        return {"converged": conv, "iterations": done, "history": hist, "x": x, "final": fin,
+                "status": status}
+
+    def true_res() -> float:
+        A.apply(x, tmp)
+        ops.axpby(1.0, bvec, -1.0, tmp)
+        return math.sqrt(_global_norm2(ops, comm, tmp, sc, 1)) / bnorm
+
+    def update_x(j, g):
+        y = np.zeros(j + 1)
+        for i in range(j, -1, -1):
+            y[i] = (g[i] - np.dot(Hh[i, i + 1:j + 1], y[i + 1:j + 1])) / Hh[i, i]
+        for i in range(j + 1):
+            ops.axpby(float(y[i]), V[i], 1.0, x)
+
+    if bnorm == 0.0:
+        if params.max_iters >= 1:
+            hist.append(0.0)
+        return out(True, 0.0)
+    if params.max_iters == 0:
+        return out(False, None)
+    while done < params.max_iters:
+        A.apply(x, tmp)
+        ops.axpby(1.0, bvec, -1.0, tmp)               # r = b - A x
+        beta = math.sqrt(_global_norm2(ops, comm, tmp, sc, 2))
+        _finite(beta, "residual norm", done)
+        if beta / bnorm <= params.tol:
+            return out(True, beta / bnorm)
+        ops.axpby(1.0 / beta, tmp, 0.0, V[0])
+        Hh[:] = 0.0
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        moved, j = False, -1
+        for j in range(m):
+            if done >= params.max_iters:
+                j -= 1
+                break
+            w = V[j + 1]
+            A.apply(V[j], w)
+            ops.dot(V[0], w, H, 0)
+            comm.allreduce(H, 0, 1)
+            for i in range(1, j + 1):                 # w -= h_{i-1} V_{i-1}; h_i = V_i . w
+                ops.axpy_dot(H, i - 1, -1.0, V[i - 1], w, V[i], H, i)
+                comm.allreduce(H, i, 1)
+            ops.axpy_dot(H, j, -1.0, V[j], w, None, H, j + 1)   # ||w||^2
+            comm.allreduce(H, j + 1, 1)
+            col = ops.read(H, j + 2)
+            Hh[:j + 1, j] = col[:j + 1]
+            hn = math.sqrt(col[j + 1])
+            _finite(hn, "Arnoldi norm", done + 1)
+            for i in range(j):
+                t = cs[i] * Hh[i, j] + sn[i] * Hh[i + 1, j]
+                Hh[i + 1, j] = -sn[i] * Hh[i, j] + cs[i] * Hh[i + 1, j]
+                Hh[i, j] = t
+            d = float(np.hypot(Hh[j, j], hn))
+            cs[j], sn[j] = (1.0, 0.0) if d == 0.0 else (Hh[j, j] / d, hn / d)
+            Hh[j, j] = cs[j] * Hh[j, j] + sn[j] * hn
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            done += 1
+            est = abs(g[j + 1]) / bnorm
+            _finite(est, "residual estimate", done)
+            hist.append(est)
+            if hn == 0.0:
+                if Hh[j, j] != 0.0:
+                    update_x(j, g)
+                fin = true_res()
+                if fin <= params.tol:
+                    return out(True, fin)
+                raise StagnationError(f"Arnoldi breakdown at iteration {done} with relative "
+                                      f"residual {fin:.3e} above tol {params.tol:.3e}")
+            if est <= params.tol:
+                update_x(j, g)
+                fin = true_res()
+                if fin <= params.tol:
+                    return out(True, fin)
+                moved = True
+                break
+            ops.scale(w, 1.0 / hn)
+        if j >= 0 and not moved:
+            update_x(j, g)
+    fin = true_res()
+    return out(fin <= params.tol, fin)
+
+
+def dist_cg(A: DistOperator, b_local, params) -> dict:
+    """Hestenes-Stiefel CG over row-partitioned vectors (oracle/cpu_oracle.py:
+    cg): one halo exchange + local SpMV and two scalar all-reduces per
+    iteration."""
+    ops, comm = A.ops, A.comm
+    x, r, p, q, bvec = ops.vec(), ops.vec(), ops.vec(), ops.vec(), ops.vec()
+    ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
+        ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
+    sc = ops.scalars(4)
+    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 0))
+    hist, done = [], 0
+
+    def out(conv, fin, status="ok"):
+        return {"converged": conv, "iterations": done, "history": hist, "x": x, "final": fin,
+                "status": status}
+
+    def true_res() -> float:
+        A.apply(x, q)
+        ops.axpby(1.0, bvec, -1.0, q)
+        ops.axpby(1.0, q, 0.0, r)
+        return math.sqrt(_global_norm2(ops, comm, r, sc, 1)) / bnorm
+
+    if bnorm == 0.0:
+        if params.max_iters >= 1:
+            hist.append(0.0)
+        return out(True, 0.0)
+    if params.max_iters == 0:
+        return out(False, None)
+    ops.axpby(1.0, bvec, 0.0, r)
+    ops.axpby(1.0, r, 0.0, p)
+    rr = _global_norm2(ops, comm, r, sc, 2)
+    while done < params.max_iters:
+        A.apply(p, q)
+        ops.dot(p, q, sc, 3)
+        comm.allreduce(sc, 3, 1)
+        pq = float(ops.read(sc, 4)[3])
+        _finite(pq, "curvature p.Ap", done + 1)
+        if pq == 0.0:
+            fin = true_res()
+            if fin <= params.tol:
+                return out(True, fin)
+            raise StagnationError(f"CG breakdown (p.Ap = 0) at iteration {done + 1} with relative "
+                                  f"residual {fin:.3e} above tol {params.tol:.3e}")
+        alpha = rr / pq
+        ops.axpby(alpha, p, 1.0, x)
+        ops.axpby(-alpha, q, 1.0, r)
+        rr_new = _global_norm2(ops, comm, r, sc, 2)
+        done += 1
+        est = math.sqrt(rr_new) / bnorm
+        _finite(est, "residual estimate", done)
+        hist.append(est)
+        if est <= params.tol:
+            fin = true_res()                      # leaves r = b - A x
+            if fin <= params.tol:
+                return out(True, fin)
+            ops.axpby(1.0, r, 0.0, p)
+            rr = _global_norm2(ops, comm, r, sc, 2)
+            continue
+        ops.axpby(1.0, r, rr_new / rr, p)
+        rr = rr_new
+    fin = true_res()
+    return out(fin <= params.tol, fin)
+
+
+# ---------------------------------------------------------------------------
+# global features for the cascade (exact aggregation across ranks)
+# ---------------------------------------------------------------------------
+def global_features(block: LocalBlock, nrows: int, ncols: int, nnz: int, comm, local_matrix,
+                    stream=None) -> FeatureVector:
+    agg = device_aggregates(local_matrix, stream)  # local rows; cols window-relative
+    # span and run lengths are translation invariant; row-length stats are exact
+    sums = comm.allgather_obj((agg[0], agg[1], agg[2], agg[3], agg[4], agg[5],
+                               block.offsets.tolist()))
+    s_r = sum(a[0] for a in sums)
+    s_r2 = sum(a[1] for a in sums)
+    mx = max(a[2] for a in sums)
+    mn = min(a[3] for a in sums)
+    span = sum(a[4] for a in sums)
+    runs = sum(a[5] for a in sums)
+    ndiag = len(set().union(*[set(a[6]) for a in sums]))
+    return features_from_aggregates(nrows, ncols, nnz, (s_r, s_r2, mx, mn, span, runs, ndiag))
+
+
+def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=None,
+                      initial_config: SpmvConfig | None = None):
+    """Row-partitioned solve under torchrun (NCCL).  Every rank passes the
+    same global host CSR; rank r keeps rows bounds[r]:bounds[r+1].  With
+    ``models`` the cascade picks the configuration from global features
+    (predict-then-solve); returns (report dict, bounds)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    n = len(row_ptr) - 1
+    bounds = partition_rows(row_ptr, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    blk = local_block(row_ptr, col_idx, values, r0, r1, n)
+    stream = device.thread_stream(+1)
+    ops, comm = CudaOps(blk.nloc, stream), NcclComm(stream)
+    cfg = initial_config or SpmvConfig(FormatTag.CSR, Library.LIB_B)
+    if models is not None:
+        from .inference import cascade_predict
+        fv = global_features(blk, n, n, int(row_ptr[-1]), comm, ops.local_csr(blk), stream)
+        cfg = cascade_predict(models, fv)
+    A = DistOperator(blk, bounds, comm, ops, cfg)
+    b_local = np.asarray(b[r0:r1], dtype=np.float64)
+    res = (dist_cg if method == "cg" else dist_gmres)(A, b_local, params)
+    res["config"] = cfg.token()
+    res["x"] = ops.fetch(res["x"])
+    return res, bounds

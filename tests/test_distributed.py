@@ -1,0 +1,197 @@
+"""Row-partitioned solver logic with world_size 2 on CPU (gloo).
+
+The distributed driver (paper_2411_10143_b200/distributed.py) is run with
+numpy/gloo doubles of its two interfaces: `ops` computes local products with
+the CPU oracle, `comm` is torch.distributed over gloo.  What is tested is the
+product's partitioning, halo plan, exchange sequencing, all-reduce placement
+and solver control flow — against the single-process oracle solve.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2411_10143_b200 import generators as G
+from paper_2411_10143_b200.distributed import (HaloPlan, dist_cg, dist_gmres, local_block,
+                                                partition_rows, DistOperator)
+from paper_2411_10143_b200.features import features_from_aggregates
+from paper_2411_10143_b200.solver import GmresParams
+from paper_2411_10143_b200.kernels import SpmvConfig
+
+
+class NumpyOps:
+    """Local-kernel test double (numpy + oracle)."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def vec(self, n=None):
+        return np.zeros(self.n if n is None else n)
+
+    def scalars(self, k):
+        return np.zeros(k)
+
+    def view(self, v, off, cnt):
+        return v[off:off + cnt]
+
+    def upload(self, v, a):
+        v[:] = a
+
+    def fetch(self, v):
+        return v.copy()
+
+    def read(self, sc, count):
+        return sc[:count].copy()
+
+    def copy(self, dst, src):
+        dst[:] = src
+
+    def dot(self, x, y, sc, i):
+        sc[i] = float(np.dot(x, y))
+
+    def axpy_dot(self, sc_a, ia, sign, x, y, z, sc_out, io):
+        y += sign * sc_a[ia] * x
+        if sc_out is not None:
+            sc_out[io] = float(np.dot(z if z is not None else y, y))
+
+    def axpby(self, a, x, b, y):
+        y[:] = a * x + b * y
+
+    def scale(self, x, s):
+        x *= s
+
+    def prepare(self, block, cfg):
+        csr = O.OCsr(block.nloc, block.window, block.row_ptr, block.cols, block.values)
+        return O.convert(csr, cfg.format.value) if cfg.format.value != "CSR" else csr
+
+    def spmv(self, mat, cfg, window, dst):
+        dst[:] = O.spmv(cfg.token(), mat, window, workers=4)
+
+
+class GlooComm:
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def allreduce(self, sc, first, count):
+        t = self.torch.from_numpy(sc[first:first + count])
+        self.dist.all_reduce(t)
+
+    def allgather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def exchange(self, sends, recvs):
+        reqs = [self.dist.isend(self.torch.from_numpy(np.ascontiguousarray(v)), p) for p, v in sends]
+        bufs = [(v, self.torch.zeros(v.size, dtype=self.torch.float64)) for _, v in recvs]
+        reqs += [self.dist.irecv(t, p) for (p, _), (_, t) in zip(recvs, bufs)]
+        for r in reqs:
+            r.wait()
+        for v, t in bufs:
+            v[:] = t.numpy()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, _, ptr, cols, vals = case["gen"]()
+        bounds = partition_rows(ptr, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        blk = local_block(ptr, cols, vals, r0, r1, n)
+        ops, comm = NumpyOps(blk.nloc), GlooComm()
+        A = DistOperator(blk, bounds, comm, ops, SpmvConfig.from_token(case["cfg"]))
+        csr = O.OCsr(n, n, ptr, cols, vals)
+        b = O.spmv_sequential(csr, np.ones(n))
+        params = GmresParams(restart_m=30, tol=1e-8, max_iters=3000)
+        res = (dist_cg if case["method"] == "cg" else dist_gmres)(A, b[r0:r1], params)
+        # global features from per-rank aggregates
+        lc = O.OCsr(blk.nloc, blk.window, blk.row_ptr, blk.cols, blk.values)
+        a = O.feature_aggregates(lc)
+        parts = comm.allgather_obj((a["sum_r"], a["sum_r2"], a["max_r"], a["min_r"], a["span"],
+                                    a["runs"], blk.offsets.tolist()))
+        agg = (sum(p[0] for p in parts), sum(p[1] for p in parts), max(p[2] for p in parts),
+               min(p[3] for p in parts), sum(p[4] for p in parts), sum(p[5] for p in parts),
+               len(set().union(*[set(p[6]) for p in parts])))
+        fv = features_from_aggregates(n, n, int(ptr[-1]), agg).to_array().tolist()
+        q.put((rank, r0, r1, res["iterations"], res["converged"], res["final"], res["x"], fv,
+               HaloPlan.build(bounds, comm.allgather_obj((blk.cmin, blk.cmax)), rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = {
+    "cg-poisson-dia": {"gen": lambda: G.poisson2d(24), "method": "cg", "cfg": "DIA/LibA"},
+    "gmres-convdiff-csr": {"gen": lambda: G.convdiff9(20), "method": "gmres", "cfg": "CSR/LibB"},
+    "gmres-powerlaw-ell": {"gen": lambda: G.powerlaw_spd(600, seed=5), "method": "gmres",
+                           "cfg": "ELL/LibA"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_row_partitioned_solve_world2(name):
+    import multiprocessing as mp
+    case = CASES[name]
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, _, ptr, cols, vals = case["gen"]()
+    csr = O.OCsr(n, n, ptr, cols, vals)
+    b = O.spmv_sequential(csr, np.ones(n))
+    mv = lambda v: O.spmv("CSR/LibB", csr, v)          # noqa: E731
+    ref = (O.cg(mv, b, tol=1e-8, max_iters=3000) if case["method"] == "cg"
+           else O.gmres(mv, b, restart=30, tol=1e-8, max_iters=3000))
+    x = np.concatenate([o[6] for o in outs])
+    assert [o[1] for o in outs] == [0, outs[0][2]] and outs[-1][2] == n
+    for o in outs:
+        assert o[3] == outs[0][3]                       # ranks agree
+        assert o[4] and o[5] <= 1e-8
+    assert abs(outs[0][3] - ref["iterations"]) <= 1
+    assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+    assert outs[0][7] == O.features(csr)                # exact global features
+    for o in outs:                                      # halo symmetric
+        plan = o[8]
+        for peer, lo, hi in plan.recvs:
+            assert (o[0], lo, hi) in [(q_, l_, h_) for q_, l_, h_ in outs[peer][8].sends]
+
+
+def test_partition_balances_nnz():
+    n, _, ptr, cols, vals = G.powerlaw_spd(5000, seed=1)
+    for world in (1, 2, 3, 8):
+        b = partition_rows(ptr, world)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        loads = np.diff(ptr[b])
+        assert loads.max() <= ptr[-1] / world + np.diff(ptr).max() + 1
+
+
+def test_stencil_halo_is_neighbour_planes():
+    n, _, ptr, cols, vals = G.laplace27(12)
+    bounds = partition_rows(ptr, 4)
+    blocks = [local_block(ptr, cols, vals, int(bounds[r]), int(bounds[r + 1]), n) for r in range(4)]
+    windows = [(b.cmin, b.cmax) for b in blocks]
+    for r in range(4):
+        plan = HaloPlan.build(bounds, windows, r)
+        peers = sorted(p for p, _, _ in plan.recvs)
+        assert peers == [p for p in (r - 1, r + 1) if 0 <= p < 4]
+        assert plan.bytes_per_exchange() <= 8 * 2 * (12 * 12 + 12 + 1)
