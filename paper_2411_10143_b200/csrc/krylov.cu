@@ -30,6 +30,8 @@ struct svb_krylov {
   int64_t chunk = 0;
   size_t res_smem = 0;
   bool resident = false;
+  bool tmem = false;        // use the TMEM-staged variant (k_gm_mgs_tmem)
+  size_t tmem_smem = 0;
   int normalized = -1;
   svb::Buf gparts;
   // recorded right after every status-producing kernel: the host waits on
@@ -545,6 +547,152 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_resident(Gm G, int j, double b
   if (lead) givens_epilogue(G, j, hnext, bnorm);
 }
 
+// ---------------------------------------------------------------------------
+// TMEM-staged SM-resident MGS (the default on sm_100a when the slice fits).
+//
+// Same pass structure as k_gm_mgs_resident, but each basis row is read from
+// HBM exactly once per Arnoldi step: pass i loads V_i's slice for the dot
+// product and parks it in tensor memory (TMEM, 256 KB/SM, otherwise idle in
+// this bandwidth-bound kernel); pass i+1 applies w -= h_i V_i from TMEM
+// instead of re-reading V_i through L2.  w stays in shared memory.  Traffic
+// per step is the algorithmic minimum 8n(j+3) bytes and L2->SM traffic is
+// halved.  TMEM layout: a thread owns TMEM lane 32*(warp%4)+lane and the 64
+// columns [64*(warp/4), +64), i.e. up to 32 doubles (elements tid+u*PB).
+// ---------------------------------------------------------------------------
+constexpr int TMEM_COLS = 512;
+constexpr int TMEM_MAX_PER_THREAD = 32;  // doubles per thread (64 columns)
+constexpr int TB = 8;                    // doubles per tcgen05 batch (.x16)
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const double* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, double* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(PB, 1) k_gm_mgs_tmem(Gm G, int j, double bnorm, int64_t chunk,
+                                                      double* gparts, unsigned* gcounter) {
+  extern __shared__ double ws[];
+  double* scratch = ws + chunk;  // 34 doubles
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // this thread's lane quadrant and column block
+  const uint32_t my_tmem = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = G.n < lo + chunk ? G.n : lo + chunk;
+  const int len = hi > lo ? (int)(hi - lo) : 0;
+  const int nbatch = (len + TB * PB - 1) / (TB * PB);   // uniform across the CTA
+  double* wg = G.V + (int64_t)(j + 1) * G.ld + lo;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  auto row = [&](int i) { return G.V + (int64_t)i * G.ld + lo; };
+
+  // pass 0: stage w in smem, V_0 in TMEM, h_0 = V_0 . w
+  double acc = 0.0;
+  if (j >= 1) prefetch_slice_l2(row(1), len);
+  {
+    const double* v0 = row(0);
+    for (int bt = 0; bt < nbatch; ++bt) {
+      double a[TB], b[TB];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const int k = threadIdx.x + (bt * TB + u) * PB;
+        a[u] = k < len ? __ldcs(wg + k) : 0.0;
+        b[u] = k < len ? __ldcs(v0 + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const int k = threadIdx.x + (bt * TB + u) * PB;
+        if (k < len) ws[k] = a[u];
+        acc += b[u] * a[u];
+      }
+      tmem_st16(my_tmem + 16 * bt, b);
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  double h = fused_grid_sum(acc, gparts, gcounter, 0, scratch);
+  if (lead) G.H[j] = h;
+
+  // passes 1..j: w -= h_{i-1} V_{i-1} (TMEM);  h_i = V_i . w;  V_i -> TMEM
+  for (int i = 1; i <= j; ++i) {
+    const double* vi = row(i);
+    if (i + 1 <= j) prefetch_slice_l2(row(i + 1), len);
+    acc = 0.0;
+    for (int bt = 0; bt < nbatch; ++bt) {
+      double b[TB], p[TB];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const int k = threadIdx.x + (bt * TB + u) * PB;
+        b[u] = k < len ? __ldcs(vi + k) : 0.0;
+      }
+      tmem_ld16(my_tmem + 16 * bt, p);
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const int k = threadIdx.x + (bt * TB + u) * PB;
+        if (k < len) {
+          const double w = ws[k] - h * p[u];
+          ws[k] = w;
+          acc += b[u] * w;
+        }
+      }
+      tmem_st16(my_tmem + 16 * bt, b);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    h = fused_grid_sum(acc, gparts, gcounter, i, scratch);
+    if (lead) G.H[i * G.m + j] = h;
+  }
+
+  // final: w -= h_j V_j (TMEM); hnext = ||w||; V[j+1] = w / hnext
+  acc = 0.0;
+  for (int bt = 0; bt < nbatch; ++bt) {
+    double p[TB];
+    tmem_ld16(my_tmem + 16 * bt, p);
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const int k = threadIdx.x + (bt * TB + u) * PB;
+      if (k < len) {
+        const double w = ws[k] - h * p[u];
+        ws[k] = w;
+        acc += w * w;
+      }
+    }
+  }
+  const double hnext = sqrt(fused_grid_sum(acc, gparts, gcounter, j + 1, scratch));
+#pragma unroll 4
+  for (int k = threadIdx.x; k < len; k += PB) wg[k] = ws[k] / hnext;
+  if (lead) givens_epilogue(G, j, hnext, bnorm);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+}
+
 // back-substitution of the rotated system (solver.py:211-214), one thread
 __global__ void k_gm_solve_y(Gm G, int j) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -824,6 +972,21 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
                                                                    k->res_smem));
         k->resident = per_sm >= 1;
         k->gparts = alloc(2 * G * sizeof(double) + 64, s);   // + grid counter
+        // TMEM-staged variant: every thread parks up to 32 doubles of V_i in
+        // TMEM; at least 120 KB of dynamic smem keeps one CTA per SM so the
+        // full 512-column TMEM allocation can never contend
+        const bool tmem_ok = !(mode && std::strcmp(mode, "resident") == 0) &&
+                             (k->chunk + PB - 1) / PB <= TMEM_MAX_PER_THREAD;
+        if (k->resident && tmem_ok) {
+          k->tmem_smem = std::max<size_t>(k->res_smem, 120 * 1024);
+          if (k->tmem_smem <= (size_t)optin) {
+            SVB_CUDA_TRY(cudaFuncSetAttribute(k_gm_mgs_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)k->tmem_smem));
+            int per = 0;
+            SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gm_mgs_tmem, PB, k->tmem_smem));
+            k->tmem = per == 1;
+          }
+        }
       }
     }
     SVB_CUDA_TRY(cudaEventCreateWithFlags(&k->ev, cudaEventDisableTiming));
@@ -916,8 +1079,12 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
       unsigned* gc = reinterpret_cast<unsigned*>(gp + 2 * sm_count());
       SVB_CUDA_TRY(cudaMemsetAsync(gc, 0, sizeof(unsigned), s));
       void* args[] = {&G, &j, &bnorm, &chunk, &gp, &gc};
-      SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_gm_mgs_resident, dim3(sm_count()), dim3(PB),
-                                               args, k->res_smem, s));
+      if (k->tmem)
+        SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_gm_mgs_tmem, dim3(sm_count()), dim3(PB), args,
+                                                 k->tmem_smem, s));
+      else
+        SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_gm_mgs_resident, dim3(sm_count()), dim3(PB),
+                                                 args, k->res_smem, s));
       note_launches(1);
       k->normalized = j;
       mark(k, s);

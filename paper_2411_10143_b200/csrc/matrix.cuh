@@ -30,6 +30,7 @@ struct svb_matrix {
   // lazily created fp32 copies of the value arrays (SVB_F32 SpMV)
   mutable std::mutex mu;
   mutable svb::Buf vals32, svals32;
+  mutable int64_t max_row_len = -1;  // CSR: longest row, computed on first need
 
   int64_t device_bytes() const {
     int64_t b = 0;

@@ -116,13 +116,48 @@ __global__ void __launch_bounds__(256) k_csr_vector(int64_t nrows, const P* __re
 // bounds and the pieces are added from 0 in chunk order.  CTAs whose rows
 // exceed the staging capacity (long rows) read their products from global.
 // ---------------------------------------------------------------------------
+// CSR-vector order for one thread: the reference's L-lane halving tree
+// (kernels.py:176-189) written as a recursion over lane subsets — the final
+// value is tree(evens) + tree(odds), recursively, and leaf t is the
+// sequential sum of elements t, t+L, ... .  Only Lp = min(L, next_pow2(len))
+// lanes are materialised: the higher lanes only ever hold +0.0 and leaves
+// are sums started from +0.0 (never -0.0), so the skipped tree steps are
+// exact no-ops.
+template <int LEVEL, class T, class G>
+__device__ __forceinline__ T lane_tree(const G& get, int64_t s, int64_t len, int L, int t, int stride) {
+  if constexpr (LEVEL == 0) {
+    T leaf = T(0);
+    for (int64_t k = t; k < len; k += L) leaf = leaf + get(s + k);
+    return leaf;
+  } else {
+    const T even = lane_tree<LEVEL - 1, T>(get, s, len, L, t, 2 * stride);
+    const T odd = lane_tree<LEVEL - 1, T>(get, s, len, L, t + stride, 2 * stride);
+    return even + odd;
+  }
+}
+
+template <class T, class G>
+__device__ __forceinline__ T lane_tree_sum(const G& get, int64_t s, int64_t len, int L) {
+  int bits = 0;
+  while ((1 << bits) < L && (1 << bits) < len) ++bits;
+  switch (bits) {
+    case 0: return lane_tree<0, T>(get, s, len, L, 0, 1);
+    case 1: return lane_tree<1, T>(get, s, len, L, 0, 1);
+    case 2: return lane_tree<2, T>(get, s, len, L, 0, 1);
+    case 3: return lane_tree<3, T>(get, s, len, L, 0, 1);
+    case 4: return lane_tree<4, T>(get, s, len, L, 0, 1);
+    default: return lane_tree<5, T>(get, s, len, L, 0, 1);
+  }
+}
+
 template <class T, class P>
 __device__ __forceinline__ T row_value(const T* sp, int64_t E0, bool staged, int64_t s, int64_t e,
                                        const int* __restrict__ cols, const T* __restrict__ vals,
                                        const T* __restrict__ x, const int64_t* __restrict__ bounds,
-                                       int nb) {
+                                       int nb, int lanes) {
   auto get_s = [&](int64_t k) { return sp[k - E0]; };
   auto get_g = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
+  if (lanes > 0) return staged ? lane_tree_sum<T>(get_s, s, e - s, lanes) : lane_tree_sum<T>(get_g, s, e - s, lanes);
   if (bounds == nullptr) {
     if (e == s) return T(0);
     return staged ? segment_sum<T>(get_s, s, e) : segment_sum<T>(get_g, s, e);
@@ -150,7 +185,8 @@ __global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const
                                                             const int* __restrict__ cols,
                                                             const T* __restrict__ vals,
                                                             const T* __restrict__ x, T* __restrict__ y,
-                                                            const int64_t* __restrict__ bounds, int nb) {
+                                                            const int64_t* __restrict__ bounds, int nb,
+                                                            int lanes) {
   __shared__ int64_t sptr[ROWSEG_ROWS + 1];
   __shared__ T sp[ROWSEG_CAP];
   const int64_t r0 = (int64_t)blockIdx.x * ROWSEG_ROWS;
@@ -182,7 +218,7 @@ __global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const
   }
   if (threadIdx.x < nr) {
     const int64_t s = sptr[threadIdx.x], e = sptr[threadIdx.x + 1];
-    y[r0 + threadIdx.x] = row_value<T, P>(sp, E0, staged, s, e, cols, vals, x, bounds, nb);
+    y[r0 + threadIdx.x] = row_value<T, P>(sp, E0, staged, s, e, cols, vals, x, bounds, nb, lanes);
   }
 }
 
@@ -443,12 +479,49 @@ void forget_bounds(const svb_matrix* m) {
     it = (it->first.first == m) ? c.map.erase(it) : std::next(it);
 }
 
+constexpr int64_t LANE_STAGED_MAX_ROW = 64;
+
+__global__ void k_row_max(int64_t nrows, const int* __restrict__ p32, const long long* __restrict__ p64,
+                          unsigned long long* out) {
+  int64_t best = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = p64 ? p64[i + 1] - p64[i] : (int64_t)p32[i + 1] - p32[i];
+    best = len > best ? len : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const int64_t other = __shfl_xor_sync(0xffffffffu, (long long)best, o);
+    best = other > best ? other : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)best);
+}
+
+// Longest row of a CSR handle, computed once and cached on the handle.
+static int64_t csr_max_row_len(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->max_row_len < 0) {
+    Buf d = alloc(8, s);
+    SVB_CUDA_TRY(cudaMemsetAsync(d->ptr, 0, 8, s));
+    k_row_max<<<grid_for(m->nrows, 256), 256, 0, s>>>(m->nrows, m->ptr64 ? nullptr : ptr<int>(m->ptr),
+                                                      m->ptr64 ? ptr<long long>(m->ptr) : nullptr,
+                                                      ptr<unsigned long long>(d));
+    SVB_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    SVB_CUDA_TRY(cudaMemcpyAsync(&h, d->ptr, 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    m->max_row_len = (int64_t)h;
+  }
+  return m->max_row_len;
+}
+
 template <class T>
 static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int workers,
                         const T* vals, const T* svals, const T* x, T* y, cudaStream_t s) {
   const int64_t n = m->nrows;
   if (fmt == SVB_CSR) {
-    if (lib == SVB_LIBA) {
+    if (lib == SVB_LIBA && !(lane == 2 || lane == 4 || lane == 8 || lane == 16 || lane == 32))
+      throw Error{SVB_UNSUPPORTED_CONFIG, "lane_width must be one of (2, 4, 8, 16, 32)"};
+    if (lib == SVB_LIBA && csr_max_row_len(m, s) > LANE_STAGED_MAX_ROW) {
+      // long rows: the warp kernel keeps L lanes per row busy
       const unsigned g = grid_for(n * lane, 256, 8);
 #define SVB_VEC(LL)                                                                        \
   case LL:                                                                                 \
@@ -465,13 +538,14 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
         SVB_VEC(8)
         SVB_VEC(16)
         SVB_VEC(32)
-        default:
-          throw Error{SVB_UNSUPPORTED_CONFIG, "lane_width must be one of (2, 4, 8, 16, 32)"};
       }
 #undef SVB_VEC
     } else {
+      // short rows (and LibB / LibC): CTA-staged rows, one thread per row,
+      // reduced in the configuration's exact order
       const int64_t* bounds = nullptr;
       int nb = 0;
+      const int lanes = lib == SVB_LIBA ? lane : 0;
       if (lib == SVB_LIBC) {
         if (m->nnz == 0) {
           SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
@@ -482,10 +556,10 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
       const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
       if (m->ptr64)
         k_csr_rowseg<T, long long><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                                             vals, x, y, bounds, nb);
+                                                             vals, x, y, bounds, nb, lanes);
       else
         k_csr_rowseg<T, int><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<int>(m->ptr), ptr<int>(m->cols), vals, x, y,
-                                                       bounds, nb);
+                                                       bounds, nb, lanes);
     }
   } else if (fmt == SVB_COO) {
     SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));

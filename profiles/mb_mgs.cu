@@ -234,6 +234,9 @@ int main() {
   cudaMalloc(&gp, 4096);
   cudaMalloc(&ctr, 64);
   cudaMalloc(&out, 4096);
+  // pure barrier cost: tiny vectors, so the pass body is negligible
+  run<true, true, false, 8>("barrier only (n=296)", V, 296, 320, 20, gp, ctr, out);
+  run<false, true, false, 8>("no barrier (n=296)", V, 296, 320, 20, gp, ctr, out);
   Part* parts;
   cudaMalloc(&parts, 2 * 148 * sizeof(Part));
   cudaMemset(parts, 0, 2 * 148 * sizeof(Part));
