@@ -242,7 +242,9 @@ def algorithmic_bytes(tag: str, info, n: int) -> float:
         return 12 * n * info["width"] + 8 * ncols + 8 * n
     if fmt == "HYB":
         return 12 * n * info["width"] + 16 * info["spill"] + 8 * ncols + 16 * n
-    return 16 * nnz + 8 * ncols + 8 * n          # COO
+    if tok.startswith("COO/LibA"):               # row kernel over cached run starts
+        return 12 * nnz + 8 * (n + 1) + 8 * ncols + 8 * n
+    return 16 * nnz + 8 * ncols + 8 * n          # COO (rows + cols + vals)
 
 
 def mgs_bytes(n: int, j: int, resident: bool = True) -> float:

@@ -140,6 +140,47 @@ __device__ __forceinline__ T pw_leaf(const G& get, int64_t lo, int64_t n) {
 // n2 = n/2 rounded down to a multiple of 8 and add the halves.  The
 // recursion is unrolled onto an explicit stack (depth <= 28 covers 2^31
 // addends) so the common short-segment path carries no call frames.
+// The same recursion with a caller-supplied leaf evaluator `leaf(lo, n)`
+// (n <= 128): used to enumerate the leaves of a long segment and later to
+// combine leaf sums computed in parallel by a warp, in identical order.
+template <class T, class L>
+__device__ T pw_traverse(const L& leaf, int64_t lo, int64_t n) {
+  if (n <= 128) return leaf(lo, n);
+  struct Frame {
+    int64_t lo, n;
+    T left;
+    int state;
+  };
+  Frame st[28];
+  int sp = 0;
+  st[0] = {lo, n, T(0), 0};
+  T ret = T(0);
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      ret = leaf(f.lo, f.n);
+      --sp;
+      continue;
+    }
+    int64_t n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[sp + 1] = {f.lo, n2, T(0), 0};
+      ++sp;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.lo + n2, f.n - n2, T(0), 0};
+      ++sp;
+    } else {
+      ret = f.left + ret;
+      --sp;
+    }
+  }
+  return ret;
+}
+
 template <class T, class G>
 __device__ T pw_sum(const G& get, int64_t lo, int64_t n) {
   if (n <= 128) return pw_leaf<T>(get, lo, n);

@@ -30,7 +30,8 @@ Buf alloc(size_t bytes, cudaStream_t s) {
   b->bytes = bytes;
   b->stream = s;
   if (bytes) {
-    cudaError_t e = cudaMallocAsync(&b->ptr, bytes, s);
+    // +128 B tail: bulk (TMA) copies round their byte counts up to 16 B
+    cudaError_t e = cudaMallocAsync(&b->ptr, bytes + 128, s);
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Error{e == cudaErrorMemoryAllocation ? SVB_OOM : SVB_CUDA,

@@ -30,7 +30,13 @@ struct svb_matrix {
   // lazily created fp32 copies of the value arrays (SVB_F32 SpMV)
   mutable std::mutex mu;
   mutable svb::Buf vals32, svals32;
-  mutable int64_t max_row_len = -1;  // CSR: longest row, computed on first need
+  // rows/runs longer than LONG_ROW (CSR rows, COO runs, HYB spill runs):
+  // (row, first entry, end) lists built on first use by the SpMV dispatcher
+  mutable int64_t nlong = -1;
+  mutable svb::Buf lrow, lbeg, lend;
+  // COO: row-run starts (int64 row pointer derived from the sorted rows —
+  // what np.flatnonzero(np.diff(rows)) computes on every reference call)
+  mutable svb::Buf dptr;
 
   int64_t device_bytes() const {
     int64_t b = 0;

@@ -8,12 +8,12 @@
 //   CSR/LibA/L   lane j%L sequential from 0, halving tree  -> warp shuffles
 //   CSR/LibB     p[s] + pairwise(p[s+1:e])                -> staged row segments
 //   CSR/LibC     per (row x chunk) segment, chunk order    -> staged row pieces
-//   COO/LibA     reduceat over row runs                    -> tile segmented reduce
+//   COO/LibA     reduceat over row runs                    -> row kernel on cached run starts
 //   COO/LibB     np.add.at, random order                   -> warp-aggregated atomics
 //   ELL/LibA     column sweep from 0                       -> thread per row
 //   ELL/LibC     S strided partials, merged in order       -> thread per row
 //   DIA/LibA     ascending-offset sweep                    -> thread per row
-//   HYB/LibA     ELL sweep, then += reduceat(spill)        -> two kernels
+//   HYB/LibA     ELL sweep, then += reduceat(spill runs)   -> ELL + row kernel (add)
 // All kernels are bandwidth-bound (~2 flop per 12-16 B): no tensor cores.
 #include <algorithm>
 #include <cmath>
@@ -26,96 +26,7 @@ namespace svb {
 
 constexpr int ROWSEG_ROWS = 128;     // rows per CTA of the staged row-segment kernel
 constexpr int ROWSEG_CAP = 2048;     // staged products per CTA
-constexpr int COO_THREADS = 128;
-constexpr int COO_ITEMS = 8;
-constexpr int COO_TILE = COO_THREADS * COO_ITEMS;
 
-// ---------------------------------------------------------------------------
-// CSR/LibA/L — CSR-vector (kernels.py:167-189)
-//
-// Reference order: lane j%L of a row accumulates elements j, j+L, ...
-// sequentially from 0, then the halving tree lanes[:h] += lanes[h:2h].
-// A warp takes a tile of 32 rows and picks the effective lane count
-// Lp = min(L, next_pow2(longest row in the tile)).  This is exact: lanes
-// >= len only ever hold +0.0, so the tree steps h >= Lp each add +0.0 —
-// the first turns a -0.0 partial into +0.0, the rest are no-ops — and the
-// remaining steps are precisely the Lp-lane tree.  Short rows therefore get
-// 32/Lp rows per warp instead of one, and U row groups are interleaved so
-// every thread keeps U independent load chains in flight.
-// ---------------------------------------------------------------------------
-template <class T, class P, int L>
-__global__ void __launch_bounds__(256) k_csr_vector(int64_t nrows, const P* __restrict__ ptr,
-                                                    const int* __restrict__ cols,
-                                                    const T* __restrict__ vals,
-                                                    const T* __restrict__ x, T* __restrict__ y) {
-  constexpr int U = 4;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t0 = warp * 32; t0 < nrows; t0 += nwarps * 32) {   // warp-uniform
-    const int64_t myrow = t0 + lane;
-    int64_t ms = 0, ml = 0;
-    if (myrow < nrows) {
-      ms = ptr[myrow];
-      ml = ptr[myrow + 1] - ms;
-    }
-    const unsigned longest = __reduce_max_sync(0xffffffffu, (unsigned)(ml < (1 << 30) ? ml : (1 << 30)));
-    int Lp = 1;
-    while (Lp < L && (unsigned)Lp < longest) Lp <<= 1;
-    const int G = 32 / Lp;          // rows per group
-    const int sub = lane & (Lp - 1);
-    const int slot = lane / Lp;
-    for (int g0 = 0; g0 < Lp; g0 += U) {   // Lp groups cover the 32-row tile
-      int64_t s[U], len[U];
-      T acc[U];
-      int64_t most = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = (g0 + u) * G + slot;           // row within the tile
-        const int src = q < 32 ? q : 0;
-        s[u] = __shfl_sync(0xffffffffu, ms, src);
-        len[u] = __shfl_sync(0xffffffffu, ml, src);
-        if (g0 + u >= Lp || q >= 32) len[u] = 0;
-        acc[u] = T(0);
-        most = len[u] > most ? len[u] : most;
-      }
-      for (int64_t t = sub; t < most; t += Lp) {
-        T v[U];
-        int c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (t < len[u]) {
-            v[u] = ld_stream(vals + s[u] + t);
-            c[u] = ld_stream(cols + s[u] + t);
-          }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (t < len[u]) acc[u] = acc[u] + v[u] * ld_x(x + c[u]);
-      }
-      if (Lp < L) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = acc[u] + T(0);
-      }
-      for (int h = Lp >> 1; h >= 1; h >>= 1) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] = acc[u] + __shfl_down_sync(0xffffffffu, acc[u], h, Lp);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = (g0 + u) * G + slot;
-        if (sub == 0 && g0 + u < Lp && q < 32 && t0 + q < nrows) y[t0 + q] = acc[u];
-      }
-    }
-  }
-}
-// ---------------------------------------------------------------------------
-// CSR/LibB (row-scalar, kernels.py:192-199) and CSR/LibC (merge-path chunks,
-// kernels.py:202-223): each CTA stages the products of its 128 rows into
-// shared memory with coalesced loads, then every thread reduces its own row
-// in the reference's reduceat order.  For LibC the row is cut at the chunk
-// bounds and the pieces are added from 0 in chunk order.  CTAs whose rows
-// exceed the staging capacity (long rows) read their products from global.
-// ---------------------------------------------------------------------------
 // CSR-vector order for one thread: the reference's L-lane halving tree
 // (kernels.py:176-189) written as a recursion over lane subsets — the final
 // value is tree(evens) + tree(odds), recursively, and leaf t is the
@@ -150,37 +61,129 @@ __device__ __forceinline__ T lane_tree_sum(const G& get, int64_t s, int64_t len,
   }
 }
 
-template <class T, class P>
-__device__ __forceinline__ T row_value(const T* sp, int64_t E0, bool staged, int64_t s, int64_t e,
-                                       const int* __restrict__ cols, const T* __restrict__ vals,
-                                       const T* __restrict__ x, const int64_t* __restrict__ bounds,
-                                       int nb, int lanes) {
-  auto get_s = [&](int64_t k) { return sp[k - E0]; };
-  auto get_g = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
-  if (lanes > 0) return staged ? lane_tree_sum<T>(get_s, s, e - s, lanes) : lane_tree_sum<T>(get_g, s, e - s, lanes);
-  if (bounds == nullptr) {
-    if (e == s) return T(0);
-    return staged ? segment_sum<T>(get_s, s, e) : segment_sum<T>(get_g, s, e);
-  }
-  // LibC: first chunk bound strictly greater than s
+// ---------------------------------------------------------------------------
+// Helpers shared by the exact row reductions
+// ---------------------------------------------------------------------------
+constexpr int LONG_ROW = 128;    // pairwise rows longer than this are reduced by a whole warp
+constexpr int LONG_LANE_ROW = 32;  // lane-tree rows longer than this likewise (L lanes, coalesced)
+constexpr int WARP_LEAVES = 64;  // leaf slots per warp for long pairwise segments
+
+// LibB: p[s] + pairwise(p[s+1:e]); LibC: the row cut at the chunk bounds,
+// each piece reduced that way and added from 0 in chunk order.
+template <class T, class G>
+__device__ __forceinline__ T pw_row_value(const G& get, int64_t s, int64_t e, const int64_t* __restrict__ bounds,
+                                          int nb) {
+  if (bounds == nullptr) return e == s ? T(0) : segment_sum<T>(get, s, e);
   int lo = 0, hi = nb;
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
+    const int mid = (lo + hi) >> 1;
     if (bounds[mid] <= s) lo = mid + 1; else hi = mid;
   }
   T acc = T(0);
-  int64_t cur = s;
-  while (cur < e) {
-    int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
-    T piece = staged ? segment_sum<T>(get_s, cur, nxt) : segment_sum<T>(get_g, cur, nxt);
-    acc = acc + piece;
+  for (int64_t cur = s; cur < e; ++lo) {
+    const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
+    acc = acc + segment_sum<T>(get, cur, nxt);
     cur = nxt;
-    ++lo;
   }
   return acc;
 }
 
-template <class T, class P>
+// Warp-cooperative p[s] + pairwise(p[s+1:e]) for one long segment: lane 0
+// enumerates the recursion's leaves, 8 lanes evaluate each leaf (one lane
+// per numpy accumulator, combined with the same ((r0+r1)+(r2+r3))+... tree),
+// then lane 0 combines the leaf sums along the recursion.  Result on lane 0.
+template <class T, class G>
+__device__ T warp_pw_segment(const G& get, int64_t s, int64_t e, int64_t* loff, int* llen, T* lsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t m = e - s - 1;  // elements of the pairwise part
+  if (m <= 0) return get(s);
+  int nleaf = 0;
+  if (lane == 0) {
+    pw_traverse<T>([&](int64_t lo, int64_t n) {
+      if (nleaf < WARP_LEAVES) {
+        loff[nleaf] = lo;
+        llen[nleaf] = (int)n;
+      }
+      ++nleaf;
+      return T(0);
+    }, s + 1, m);
+  }
+  nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
+  if (nleaf > WARP_LEAVES) {  // extremely long segment: sequential fallback
+    T r = T(0);
+    if (lane == 0) r = segment_sum<T>(get, s, e);
+    return r;
+  }
+  __syncwarp();
+  const int grp = lane >> 3, k = lane & 7;
+  for (int l0 = 0; l0 < nleaf; l0 += 4) {
+    const int li = l0 + grp;
+    T r = T(0);
+    int64_t lo = 0;
+    int n = 0;
+    if (li < nleaf) {
+      lo = loff[li];
+      n = llen[li];
+    }
+    if (n >= 8) {
+      r = get(lo + k);
+      const int lim = n - (n % 8);
+      for (int i = 8; i < lim; i += 8) r = r + get(lo + i + k);
+    }
+    // fixed combine tree inside each 8-lane group
+    T o = __shfl_down_sync(0xffffffffu, r, 1);
+    if ((k & 1) == 0) r = r + o;
+    o = __shfl_down_sync(0xffffffffu, r, 2);
+    if ((k & 3) == 0) r = r + o;
+    o = __shfl_down_sync(0xffffffffu, r, 4);
+    if (k == 0) r = r + o;
+    if (k == 0 && li < nleaf) {
+      if (n < 8) {
+        T q = T(-0.0);
+        for (int i = 0; i < n; ++i) q = q + get(lo + i);
+        r = q;
+      } else {
+        for (int i = n - (n % 8); i < n; ++i) r = r + get(lo + i);
+      }
+      lsum[li] = r;
+    }
+  }
+  __syncwarp();
+  T total = T(0);
+  if (lane == 0) {
+    int next = 0;
+    total = pw_traverse<T>([&](int64_t, int64_t) { return lsum[next++]; }, s + 1, m);
+    total = get(s) + total;
+  }
+  return total;
+}
+
+// Warp-cooperative L-lane CSR-vector row (len > LONG_ROW >= L): lane t < L
+// sums elements t, t+L, ... in order; halving tree.  Result on lane 0.
+template <class T, class G>
+__device__ T warp_lane_row(const G& get, int64_t s, int64_t len, int L) {
+  const int lane = threadIdx.x & 31;
+  T acc = T(0);
+  if (lane < L)
+    for (int64_t k = lane; k < len; k += L) acc = acc + get(s + k);
+  for (int h = L >> 1; h >= 1; h >>= 1) {
+    const T o = __shfl_down_sync(0xffffffffu, acc, h);
+    if (lane < h) acc = acc + o;
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// CSR/LibA/L (kernels.py:167-189), CSR/LibB (kernels.py:192-199) and
+// CSR/LibC (kernels.py:202-223).  Each CTA owns 128 consecutive rows; all
+// threads stage the rows' products p = v*x[c] in shared memory with
+// coalesced loads and U independent gathers in flight per thread; then one
+// thread per row reduces it in the configuration's exact order (lane tree,
+// numpy pairwise, or chunk pieces) and rows longer than LONG_ROW are reduced
+// by a whole warp (leaf-parallel pairwise / L lanes).  CTAs whose entries
+// exceed the staging capacity read their products from global memory.
+// ---------------------------------------------------------------------------
+template <class T, class P, bool ADD>
 __global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const P* __restrict__ ptr,
                                                             const int* __restrict__ cols,
                                                             const T* __restrict__ vals,
@@ -189,15 +192,17 @@ __global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const
                                                             int lanes) {
   __shared__ int64_t sptr[ROWSEG_ROWS + 1];
   __shared__ T sp[ROWSEG_CAP];
+  const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * ROWSEG_ROWS;
   const int nr = (int)(nrows - r0 < ROWSEG_ROWS ? nrows - r0 : ROWSEG_ROWS);
-  for (int i = threadIdx.x; i <= nr; i += blockDim.x) sptr[i] = ptr[r0 + i];
+  for (int i = tid; i <= nr; i += blockDim.x) sptr[i] = ptr[r0 + i];
   __syncthreads();
-  const int64_t E0 = sptr[0], E1 = sptr[nr];
-  const bool staged = (E1 - E0) <= ROWSEG_CAP;
-  if (staged) {
+  const int64_t E0 = sptr[0];
+  // stage the CTA's products (a prefix when long rows push it past capacity)
+  const int64_t E1 = sptr[nr] - E0 <= ROWSEG_CAP ? sptr[nr] : E0 + ROWSEG_CAP;
+  {
     constexpr int U = 4;
-    for (int64_t k = E0 + threadIdx.x; k < E1; k += (int64_t)ROWSEG_ROWS * U) {
+    for (int64_t k = E0 + tid; k < E1; k += (int64_t)ROWSEG_ROWS * U) {
       T v[U];
       int c[U];
 #pragma unroll
@@ -216,65 +221,65 @@ __global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const
     }
     __syncthreads();
   }
-  if (threadIdx.x < nr) {
-    const int64_t s = sptr[threadIdx.x], e = sptr[threadIdx.x + 1];
-    y[r0 + threadIdx.x] = row_value<T, P>(sp, E0, staged, s, e, cols, vals, x, bounds, nb, lanes);
+  auto get_s = [&](int64_t k) { return sp[k - E0]; };
+  auto get_g = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
+  if (tid < nr) {
+    const int64_t s = sptr[tid], e = sptr[tid + 1];
+    if (e - s <= (lanes > 0 ? LONG_LANE_ROW : LONG_ROW)) {
+      const bool staged = e <= E1;
+      T v;
+      if (lanes > 0) v = staged ? lane_tree_sum<T>(get_s, s, e - s, lanes) : lane_tree_sum<T>(get_g, s, e - s, lanes);
+      else v = staged ? pw_row_value<T>(get_s, s, e, bounds, nb) : pw_row_value<T>(get_g, s, e, bounds, nb);
+      if (!ADD) y[r0 + tid] = v;
+      else if (e > s) y[r0 + tid] = y[r0 + tid] + v;   // HYB spill: rows with entries only
+    }
   }
+  // rows longer than LONG_ROW are reduced by k_long_rows
 }
-
 // ---------------------------------------------------------------------------
-// COO/LibA (kernels.py:146-153) and the HYB spill (kernels.py:267-271):
-// tile-per-CTA segmented reduction over row-sorted coordinates.  A segment
-// (row run) belongs to the tile holding its head; runs crossing the tile end
-// continue from global memory.  ADD accumulates into y (HYB), otherwise y
-// must be zero-filled beforehand (rows without entries stay 0).
+// Long rows / runs (> LONG_ROW entries) of any row-sorted layout: one warp
+// per segment from a per-handle list, so the few heavy rows of a power-law
+// matrix run side by side instead of serialising inside one CTA.  Exact
+// order as the thread path (lane tree / pairwise / chunk pieces).
 // ---------------------------------------------------------------------------
 template <class T, bool ADD>
-__global__ void __launch_bounds__(COO_THREADS) k_coo_segreduce(int64_t nnz,
-                                                               const int* __restrict__ rows,
-                                                               const int* __restrict__ cols,
-                                                               const T* __restrict__ vals,
-                                                               const T* __restrict__ x,
-                                                               T* __restrict__ y) {
-  __shared__ int srow[COO_TILE];
-  __shared__ T sp[COO_TILE];
-  const int64_t t0 = (int64_t)blockIdx.x * COO_TILE;
-  const int n = (int)(nnz - t0 < COO_TILE ? nnz - t0 : COO_TILE);
-  {
-    T v[COO_ITEMS];
-    int c[COO_ITEMS];
-#pragma unroll
-    for (int u = 0; u < COO_ITEMS; ++u) {
-      const int k = threadIdx.x + u * COO_THREADS;
-      if (k < n) {
-        v[u] = ld_stream(vals + t0 + k);
-        c[u] = ld_stream(cols + t0 + k);
-        srow[k] = ld_stream(rows + t0 + k);
+__global__ void __launch_bounds__(128) k_long_rows(int64_t nlong, const int* __restrict__ lrow,
+                                                   const int64_t* __restrict__ lbeg, const int64_t* __restrict__ lend,
+                                                   const int* __restrict__ cols, const T* __restrict__ vals,
+                                                   const T* __restrict__ x, T* __restrict__ y,
+                                                   const int64_t* __restrict__ bounds, int nb, int lanes) {
+  __shared__ int64_t loff[4][WARP_LEAVES];
+  __shared__ int llen[4][WARP_LEAVES];
+  __shared__ T lsum[4][WARP_LEAVES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto get = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
+  for (int64_t i = (int64_t)blockIdx.x * 4 + warp; i < nlong; i += (int64_t)gridDim.x * 4) {
+    const int64_t s = lbeg[i], e = lend[i];
+    if (lanes == 0 && e - s <= LONG_ROW) continue;   // done by the thread path
+    T v;
+    if (lanes > 0) {
+      v = warp_lane_row<T>(get, s, e - s, lanes);
+    } else if (bounds == nullptr) {
+      v = warp_pw_segment<T>(get, s, e, loff[warp], llen[warp], lsum[warp]);
+    } else {
+      int lo = 0, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (bounds[mid] <= s) lo = mid + 1; else hi = mid;
       }
+      T acc = T(0);
+      for (int64_t cur = s; cur < e; ++lo) {
+        const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
+        const T piece = warp_pw_segment<T>(get, cur, nxt, loff[warp], llen[warp], lsum[warp]);
+        acc = acc + piece;
+        cur = nxt;
+      }
+      v = acc;
     }
-#pragma unroll
-    for (int u = 0; u < COO_ITEMS; ++u) {
-      const int k = threadIdx.x + u * COO_THREADS;
-      if (k < n) sp[k] = v[u] * ld_x(x + c[u]);
+    if (lane == 0) {
+      if (ADD) y[lrow[i]] = y[lrow[i]] + v;
+      else y[lrow[i]] = v;
     }
-  }
-  __syncthreads();
-  const int64_t t1 = t0 + n;
-  auto get = [&](int64_t g) {
-    return g < t1 ? sp[g - t0] : ld_stream(vals + g) * ld_x(x + ld_stream(cols + g));
-  };
-  for (int k = threadIdx.x; k < n; k += COO_THREADS) {
-    const int row = srow[k];
-    const int prev = k > 0 ? srow[k - 1] : (t0 > 0 ? rows[t0 - 1] : -1);
-    if (row == prev) continue;
-    int e = k + 1;
-    while (e < n && srow[e] == row) ++e;
-    int64_t gend = t0 + e;
-    if (e == n)
-      while (gend < nnz && rows[gend] == row) ++gend;
-    const T val = segment_sum<T>(get, t0 + k, gend);
-    if (ADD) y[row] = y[row] + val;
-    else y[row] = val;
   }
 }
 
@@ -479,38 +484,76 @@ void forget_bounds(const svb_matrix* m) {
     it = (it->first.first == m) ? c.map.erase(it) : std::next(it);
 }
 
-constexpr int64_t LANE_STAGED_MAX_ROW = 64;
-
-__global__ void k_row_max(int64_t nrows, const int* __restrict__ p32, const long long* __restrict__ p64,
-                          unsigned long long* out) {
-  int64_t best = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t len = p64 ? p64[i + 1] - p64[i] : (int64_t)p32[i + 1] - p32[i];
-    best = len > best ? len : best;
+// COO run starts as an int64 row pointer, derived once per handle
+static const long long* coo_runs(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (!m->dptr) {
+    m->dptr = rows_to_ptr(ptr<int32_t>(m->rows), m->nnz, m->nrows, true, s);
+    detach(m->dptr);
   }
-  for (int o = 16; o; o >>= 1) {
-    const int64_t other = __shfl_xor_sync(0xffffffffu, (long long)best, o);
-    best = other > best ? other : best;
-  }
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)best);
+  return ptr<long long>(m->dptr);
 }
 
-// Longest row of a CSR handle, computed once and cached on the handle.
-static int64_t csr_max_row_len(const svb_matrix* m, cudaStream_t s) {
-  std::lock_guard<std::mutex> lk(m->mu);
-  if (m->max_row_len < 0) {
-    Buf d = alloc(8, s);
-    SVB_CUDA_TRY(cudaMemsetAsync(d->ptr, 0, 8, s));
-    k_row_max<<<grid_for(m->nrows, 256), 256, 0, s>>>(m->nrows, m->ptr64 ? nullptr : ptr<int>(m->ptr),
-                                                      m->ptr64 ? ptr<long long>(m->ptr) : nullptr,
-                                                      ptr<unsigned long long>(d));
-    SVB_CHECK_LAUNCH();
-    unsigned long long h = 0;
-    SVB_CUDA_TRY(cudaMemcpyAsync(&h, d->ptr, 8, cudaMemcpyDeviceToHost, s));
-    SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    m->max_row_len = (int64_t)h;
+// rows of a row pointer longer than LONG_LANE_ROW -> (row, begin, end) list
+template <class P>
+__global__ void k_find_long(int64_t nrows, const P* __restrict__ ptr, unsigned long long* count, int* lrow,
+                            int64_t* lbeg, int64_t* lend) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = ptr[i], e = ptr[i + 1];
+    if (e - b > LONG_LANE_ROW) {
+      const unsigned long long k = atomicAdd(count, 1ull);
+      lrow[k] = (int)i;
+      lbeg[k] = b;
+      lend[k] = e;
+    }
   }
-  return m->max_row_len;
+}
+
+// The handle's long-segment list (built once, cached): CSR rows, COO runs
+// (via a derived row pointer) or the HYB spill runs.
+static int64_t long_list(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->nlong >= 0) return m->nlong;
+  const int64_t entries = m->fmt == SVB_HYB ? m->spill_nnz : m->nnz;
+  const int64_t cap = entries / (LONG_LANE_ROW + 1) + 1;
+  m->lrow = alloc(cap * 4, s);
+  m->lbeg = alloc(cap * 8, s);
+  m->lend = alloc(cap * 8, s);
+  detach(m->lrow);
+  detach(m->lbeg);
+  detach(m->lend);
+  Buf cnt = alloc(8, s);
+  SVB_CUDA_TRY(cudaMemsetAsync(cnt->ptr, 0, 8, s));
+  const unsigned g = grid_for(m->nrows, 256);
+  auto run = [&](auto* p) {
+    k_find_long<<<g, 256, 0, s>>>(m->nrows, p, ptr<unsigned long long>(cnt), ptr<int>(m->lrow),
+                                  ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend));
+    SVB_CHECK_LAUNCH();
+  };
+  if (m->fmt == SVB_CSR) {
+    if (m->ptr64) run(ptr<long long>(m->ptr));
+    else run(ptr<int>(m->ptr));
+  } else if (m->fmt == SVB_COO) {
+    run(ptr<long long>(m->dptr));
+  } else {  // HYB: spill row pointer (int64)
+    run(ptr<long long>(m->ptr));
+  }
+  unsigned long long h = 0;
+  SVB_CUDA_TRY(cudaMemcpyAsync(&h, cnt->ptr, 8, cudaMemcpyDeviceToHost, s));
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  m->nlong = (int64_t)h;
+  return m->nlong;
+}
+
+template <class T, bool ADD>
+static void launch_long(const svb_matrix* m, const int* cols, const T* vals, const T* x, T* y,
+                        const int64_t* bounds, int nb, int lanes, cudaStream_t s) {
+  const int64_t nl = long_list(m, s);
+  if (nl <= 0) return;
+  const unsigned g = (unsigned)((nl + 3) / 4);
+  k_long_rows<T, ADD><<<g, 128, 0, s>>>(nl, ptr<int>(m->lrow), ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend),
+                                        cols, vals, x, y, bounds, nb, lanes);
+  SVB_CHECK_LAUNCH();
 }
 
 template <class T>
@@ -520,55 +563,38 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
   if (fmt == SVB_CSR) {
     if (lib == SVB_LIBA && !(lane == 2 || lane == 4 || lane == 8 || lane == 16 || lane == 32))
       throw Error{SVB_UNSUPPORTED_CONFIG, "lane_width must be one of (2, 4, 8, 16, 32)"};
-    if (lib == SVB_LIBA && csr_max_row_len(m, s) > LANE_STAGED_MAX_ROW) {
-      // long rows: the warp kernel keeps L lanes per row busy
-      const unsigned g = grid_for(n * lane, 256, 8);
-#define SVB_VEC(LL)                                                                        \
-  case LL:                                                                                 \
-    if (m->ptr64)                                                                          \
-      k_csr_vector<T, long long, LL><<<g, 256, 0, s>>>(n, ptr<long long>(m->ptr),          \
-                                                       ptr<int>(m->cols), vals, x, y);     \
-    else                                                                                   \
-      k_csr_vector<T, int, LL><<<g, 256, 0, s>>>(n, ptr<int>(m->ptr), ptr<int>(m->cols),   \
-                                                 vals, x, y);                              \
-    break;
-      switch (lane) {
-        SVB_VEC(2)
-        SVB_VEC(4)
-        SVB_VEC(8)
-        SVB_VEC(16)
-        SVB_VEC(32)
+    const int64_t* bounds = nullptr;
+    int nb = 0;
+    const int lanes = lib == SVB_LIBA ? lane : 0;
+    if (lib == SVB_LIBC) {
+      if (m->nnz == 0) {
+        SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
+        return;
       }
-#undef SVB_VEC
-    } else {
-      // short rows (and LibB / LibC): CTA-staged rows, one thread per row,
-      // reduced in the configuration's exact order
-      const int64_t* bounds = nullptr;
-      int nb = 0;
-      const int lanes = lib == SVB_LIBA ? lane : 0;
-      if (lib == SVB_LIBC) {
-        if (m->nnz == 0) {
-          SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
-          return;
-        }
-        bounds = device_bounds(m, workers, &nb, s);
-      }
-      const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
-      if (m->ptr64)
-        k_csr_rowseg<T, long long><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                                             vals, x, y, bounds, nb, lanes);
-      else
-        k_csr_rowseg<T, int><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<int>(m->ptr), ptr<int>(m->cols), vals, x, y,
-                                                       bounds, nb, lanes);
+      bounds = device_bounds(m, workers, &nb, s);
     }
+    const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
+    if (m->ptr64)
+      k_csr_rowseg<T, long long, false><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->cols),
+                                                                  vals, x, y, bounds, nb, lanes);
+    else
+      k_csr_rowseg<T, int, false><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<int>(m->ptr), ptr<int>(m->cols), vals, x, y,
+                                                            bounds, nb, lanes);
+    SVB_CUDA_TRY(cudaGetLastError());   // counted by the final check below
+    launch_long<T, false>(m, ptr<int>(m->cols), vals, x, y, bounds, nb, lanes, s);
   } else if (fmt == SVB_COO) {
-    SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
-    if (m->nnz == 0) return;
     if (lib == SVB_LIBA) {
-      const unsigned g = (unsigned)((m->nnz + COO_TILE - 1) / COO_TILE);
-      k_coo_segreduce<T, false><<<g, COO_THREADS, 0, s>>>(m->nnz, ptr<int>(m->rows), ptr<int>(m->cols),
-                                                          vals, x, y);
+      // row runs of the sorted coordinates (kernels.py:141-153), reduced in
+      // reduceat order by the row kernel; rows without entries get 0
+      const long long* runs = coo_runs(m, s);
+      const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
+      k_csr_rowseg<T, long long, false><<<g, ROWSEG_ROWS, 0, s>>>(n, runs, ptr<int>(m->cols), vals, x, y,
+                                                                  nullptr, 0, 0);
+      SVB_CUDA_TRY(cudaGetLastError());
+      launch_long<T, false>(m, ptr<int>(m->cols), vals, x, y, nullptr, 0, 0, s);
     } else {
+      SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
+      if (m->nnz == 0) return;
       k_coo_atomic<T><<<grid_for(m->nnz, 256, 16), 256, 0, s>>>(m->nnz, ptr<int>(m->rows),
                                                                ptr<int>(m->cols), vals, x, y);
     }
@@ -586,9 +612,11 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
     k_ell_sweep<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), vals, x, y);
     if (m->spill_nnz > 0) {
       SVB_CHECK_LAUNCH();
-      const unsigned g = (unsigned)((m->spill_nnz + COO_TILE - 1) / COO_TILE);
-      k_coo_segreduce<T, true><<<g, COO_THREADS, 0, s>>>(m->spill_nnz, ptr<int>(m->rows),
-                                                         ptr<int>(m->scols), svals, x, y);
+      const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
+      k_csr_rowseg<T, long long, true><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->scols),
+                                                                 svals, x, y, nullptr, 0, 0);
+      SVB_CUDA_TRY(cudaGetLastError());
+      launch_long<T, true>(m, ptr<int>(m->scols), svals, x, y, nullptr, 0, 0, s);
     }
   }
   SVB_CHECK_LAUNCH();

@@ -26,7 +26,12 @@ from . import _lib
 from .errors import FormatInapplicableError  # noqa: F401  (re-export parity)
 
 DIA_OFFSET_CAP = 4096          # formats.py:18
-ELL_CELL_CAP = 1 << 33         # device memory guard for ELL/HYB (absent in the reference)
+# Device memory guard for ELL (absent in the reference, SURVEY.md §7 hard
+# part 4): a padded layout may use at most max(2^26, 8 * nnz) cells, so a
+# power-law matrix whose longest row is 200x the mean is "inapplicable"
+# instead of allocating tens of GB of padding.
+ELL_MIN_CELLS = 1 << 26
+ELL_PAD_FACTOR = 8
 
 
 class FormatTag(str, Enum):
@@ -474,7 +479,9 @@ def convert(m, target: FormatTag, *, stream=None):
     and for ELL/HYB layouts beyond the device cell cap."""
     target = FormatTag(target)
     format_of(m)
-    dev = _new_handle(_lib.lib().svb_convert, m._device().handle, _TAG_CODE[target], ELL_CELL_CAP,
+    src = m._device()
+    cap = max(ELL_MIN_CELLS, ELL_PAD_FACTOR * int(src.info.nnz))
+    dev = _new_handle(_lib.lib().svb_convert, src.handle, _TAG_CODE[target], cap,
                       stream)
     return _CLASS_OF[target]._wrap(dev)
 

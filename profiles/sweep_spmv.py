@@ -1,0 +1,96 @@
+"""SpMV roofline sweep: every configuration on the BASELINE stencil matrices
+(and a power-law matrix), device time per launch from CUDA events on the
+launching stream, achieved GB/s from the algorithmic bytes of SURVEY.md §8(d)
+against the measured HBM copy peak.
+
+    python profiles/sweep_spmv.py [runs] > profiles/r1_spmv_sweep.json
+"""
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2411_10143_b200 as P  # noqa: E402
+from paper_2411_10143_b200 import device, generators as G  # noqa: E402
+from paper_2411_10143_b200.kernels import launch  # noqa: E402
+
+RUNS = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+    if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+
+
+def alg_bytes(fmt, rep, n, ncols, lib=""):
+    inf = rep._device().info
+    if fmt == "CSR":
+        return 12 * inf.nnz + 4 * (n + 1) + 8 * ncols + 8 * n
+    if fmt == "COO" and lib == "LibA":
+        return 12 * inf.nnz + 8 * (n + 1) + 8 * ncols + 8 * n
+    if fmt == "COO":
+        return 16 * inf.nnz + 8 * ncols + 8 * n
+    if fmt == "ELL":
+        return 12 * n * inf.width + 8 * ncols + 8 * n
+    if fmt == "DIA":
+        return 8 * inf.ndiag * n + 8 * ncols + 8 * n
+    return 12 * n * inf.width + 16 * inf.spill_nnz + 8 * ncols + 16 * n
+
+
+def stencil(kind):
+    if kind == "poisson1024":
+        return P.CsrMatrix.stencil((1024, 1024), [(0, 0), (0, -1), (0, 1), (-1, 0), (1, 0)],
+                                   [4.0, -1, -1, -1, -1])
+    offs, w = [], []
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            offs.append((dy, dx))
+            w.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
+    return P.CsrMatrix.stencil((2000, 2000), offs, w)
+
+
+def main():
+    mats = {"config1_poisson1024": stencil("poisson1024"), "config2_convdiff2000": stencil("cd"),
+            "powerlaw_2M": P.CsrMatrix(*G.powerlaw_spd(2_000_000, seed=0))}
+    s = device.thread_stream()
+    ext = torch.cuda.ExternalStream(s.handle)
+    out = {"peak_gbs": PEAK, "runs": RUNS, "results": {}}
+    for name, A in mats.items():
+        n = A.nrows
+        x = device.DeviceVector.from_numpy(np.random.default_rng(0).uniform(0.5, 1.5, n), s)
+        y = device.DeviceVector(n)
+        res = {}
+        reps = {}
+        for cfg in P.enumerate_configs():
+            f = cfg.format
+            if f not in reps:
+                try:
+                    reps[f] = A if f is P.FormatTag.CSR else P.convert(A, f)
+                except (P.FormatInapplicableError, MemoryError) as exc:
+                    reps[f] = None
+                    res[f.value] = f"inapplicable: {exc}"[:120]
+            rep = reps[f]
+            if rep is None:
+                continue
+            for _ in range(3):
+                launch(cfg, rep, x.ptr, y.ptr, workers=4, stream=s)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            for _ in range(RUNS):
+                launch(cfg, rep, x.ptr, y.ptr, workers=4, stream=s)
+            e1.record(ext)
+            e1.synchronize()
+            us = e0.elapsed_time(e1) / RUNS * 1e3
+            b = alg_bytes(f.value, rep, n, n, cfg.library.value if hasattr(cfg.library, "value") else str(cfg.library))
+            res[cfg.token()] = {"us": round(us, 2), "alg_MB": round(b / 1e6, 1),
+                                "gbs": round(b / us / 1e3, 1), "frac": round(b / us / 1e3 / PEAK, 3)}
+        out["results"][name] = {"n": n, "nnz": A.nnz, "configs": res}
+        print(name, json.dumps(res), file=sys.stderr, flush=True)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
