@@ -136,16 +136,14 @@ __device__ __forceinline__ T pw_leaf(const G& get, int64_t lo, int64_t n) {
   return res;
 }
 
-// Full numpy pairwise sum: n <= 128 is a leaf, otherwise split at
-// n2 = n/2 rounded down to a multiple of 8 and add the halves.  The
-// recursion is unrolled onto an explicit stack (depth <= 28 covers 2^31
-// addends) so the common short-segment path carries no call frames.
-// The same recursion with a caller-supplied leaf evaluator `leaf(lo, n)`
-// (n <= 128): used to enumerate the leaves of a long segment and later to
-// combine leaf sums computed in parallel by a warp, in identical order.
+// numpy's pairwise recursion with a caller-supplied evaluator `leaf(lo, n)` for the
+// nodes of at most `span` addends (span >= 128; the split rule is numpy's at
+// every level): used to enumerate the leaves of a long segment and later to
+// combine leaf sums computed in parallel by a warp, in identical order, and
+// to walk the top of very long segments in warp-sized subtrees.
 template <class T, class L>
-__device__ T pw_traverse(const L& leaf, int64_t lo, int64_t n) {
-  if (n <= 128) return leaf(lo, n);
+__device__ T pw_traverse(const L& leaf, int64_t lo, int64_t n, int64_t span = 128) {
+  if (n <= span) return leaf(lo, n);
   struct Frame {
     int64_t lo, n;
     T left;
@@ -157,7 +155,7 @@ __device__ T pw_traverse(const L& leaf, int64_t lo, int64_t n) {
   T ret = T(0);
   while (sp >= 0) {
     Frame& f = st[sp];
-    if (f.n <= 128) {
+    if (f.n <= span) {
       ret = leaf(f.lo, f.n);
       --sp;
       continue;
@@ -181,6 +179,10 @@ __device__ T pw_traverse(const L& leaf, int64_t lo, int64_t n) {
   return ret;
 }
 
+// Full numpy pairwise sum: n <= 128 is a leaf, otherwise split at
+// n2 = n/2 rounded down to a multiple of 8 and add the halves.  The
+// recursion is unrolled onto an explicit stack (depth <= 28 covers 2^31
+// addends) so the common short-segment path carries no call frames.
 template <class T, class G>
 __device__ T pw_sum(const G& get, int64_t lo, int64_t n) {
   if (n <= 128) return pw_leaf<T>(get, lo, n);
@@ -255,6 +257,60 @@ __device__ __forceinline__ long long ld_stream(const long long* p) {
 template <class T>
 __device__ __forceinline__ T ld_x(const T* p) {
   return __ldg(p);
+}
+
+// ---------------------------------------------------------------------------
+// 1-D bulk copies (TMA engine, no tensor map) into shared memory, completed
+// on an mbarrier: one elected thread arms the barrier with the byte count and
+// issues the copies; every thread waits on the phase parity.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-B aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// the same with an L2 eviction-priority hint (createpolicy): streamed matrix
+// arrays are marked evict-first so the gathered x vector stays L2-resident
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// order earlier generic-proxy accesses of shared memory before later bulk
+// copies into it (buffer reuse)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 }  // namespace svb

@@ -34,6 +34,10 @@ struct svb_matrix {
   // (row, first entry, end) lists built on first use by the SpMV dispatcher
   mutable int64_t nlong = -1;
   mutable svb::Buf lrow, lbeg, lend;
+  // row tiles of the staged row kernel (spmv.cu RowTile), built on first use
+  mutable int64_t ntiles = -1;
+  mutable int tile_cap = 0;  // entry capacity the tiles were cut for
+  mutable svb::Buf tiles;
   // COO: row-run starts (int64 row pointer derived from the sorted rows —
   // what np.flatnonzero(np.diff(rows)) computes on every reference call)
   mutable svb::Buf dptr;

@@ -17,6 +17,8 @@
 // All kernels are bandwidth-bound (~2 flop per 12-16 B): no tensor cores.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 #include <map>
 #include <vector>
 
@@ -24,63 +26,85 @@
 
 namespace svb {
 
-constexpr int ROWSEG_ROWS = 128;     // rows per CTA of the staged row-segment kernel
-constexpr int ROWSEG_CAP = 2048;     // staged products per CTA
+constexpr int ROWSEG_ROWS = 128;     // threads of the row kernel = max rows per tile
 
 // CSR-vector order for one thread: the reference's L-lane halving tree
-// (kernels.py:176-189) written as a recursion over lane subsets — the final
-// value is tree(evens) + tree(odds), recursively, and leaf t is the
-// sequential sum of elements t, t+L, ... .  Only Lp = min(L, next_pow2(len))
-// lanes are materialised: the higher lanes only ever hold +0.0 and leaves
-// are sums started from +0.0 (never -0.0), so the skipped tree steps are
-// exact no-ops.
-template <int LEVEL, class T, class G>
-__device__ __forceinline__ T lane_tree(const G& get, int64_t s, int64_t len, int L, int t, int stride) {
-  if constexpr (LEVEL == 0) {
-    T leaf = T(0);
-    for (int64_t k = t; k < len; k += L) leaf = leaf + get(s + k);
-    return leaf;
-  } else {
-    const T even = lane_tree<LEVEL - 1, T>(get, s, len, L, t, 2 * stride);
-    const T odd = lane_tree<LEVEL - 1, T>(get, s, len, L, t + stride, 2 * stride);
-    return even + odd;
+// (kernels.py:176-189).  Leaf t is the sequential sum (from +0.0) of
+// elements t, t+L, ...; the halving tree over the leaves equals a balanced
+// binary tree over the leaves in bit-reversed order, evaluated here as a
+// binary counter over compile-time leaf indices (registers only).  LP leaves
+// are materialised, LP a power of two with min(L, next_pow2(len)) <= LP <= L:
+// the skipped leaves are empty sums (+0.0) and no partial sum is ever -0.0,
+// so the skipped tree steps are exact no-ops.
+__host__ __device__ constexpr int bit_reverse(int r, int nbits) {
+  int t = 0;
+  for (int b = 0; b < nbits; ++b) t |= ((r >> b) & 1) << (nbits - 1 - b);
+  return t;
+}
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+template <int LP, class T, class G>
+__device__ __forceinline__ T lane_tree_fixed(const G& get, int len, int L) {
+  constexpr int LOG = ilog2(LP);
+  T lvl[LOG + 1];
+#pragma unroll
+  for (int r = 0; r < LP; ++r) {
+    const int t = bit_reverse(r, LOG);
+    T cur = T(0);
+    for (int k = t; k < len; k += L) cur = cur + get(k);
+    int level = 0;
+#pragma unroll
+    for (int b = 0; b < LOG; ++b) {
+      if (((r + 1) >> b) & 1) break;
+      cur = lvl[b] + cur;
+      level = b + 1;
+    }
+    lvl[level] = cur;
   }
+  return lvl[LOG];
 }
 
+// Warp-uniform dispatch: LP = min(L, next_pow2(longest row of the warp)).
 template <class T, class G>
-__device__ __forceinline__ T lane_tree_sum(const G& get, int64_t s, int64_t len, int L) {
-  int bits = 0;
-  while ((1 << bits) < L && (1 << bits) < len) ++bits;
-  switch (bits) {
-    case 0: return lane_tree<0, T>(get, s, len, L, 0, 1);
-    case 1: return lane_tree<1, T>(get, s, len, L, 0, 1);
-    case 2: return lane_tree<2, T>(get, s, len, L, 0, 1);
-    case 3: return lane_tree<3, T>(get, s, len, L, 0, 1);
-    case 4: return lane_tree<4, T>(get, s, len, L, 0, 1);
-    default: return lane_tree<5, T>(get, s, len, L, 0, 1);
+__device__ __forceinline__ T lane_tree_warp(const G& get, int len, int L, int warp_max_len) {
+  int lp = 1;
+  while (lp < L && lp < warp_max_len) lp <<= 1;
+  switch (lp) {
+    case 1: return lane_tree_fixed<1, T>(get, len, L);
+    case 2: return lane_tree_fixed<2, T>(get, len, L);
+    case 4: return lane_tree_fixed<4, T>(get, len, L);
+    case 8: return lane_tree_fixed<8, T>(get, len, L);
+    case 16: return lane_tree_fixed<16, T>(get, len, L);
+    default: return lane_tree_fixed<32, T>(get, len, L);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Helpers shared by the exact row reductions
 // ---------------------------------------------------------------------------
-constexpr int LONG_ROW = 128;    // pairwise rows longer than this are reduced by a whole warp
-constexpr int LONG_LANE_ROW = 32;  // lane-tree rows longer than this likewise (L lanes, coalesced)
-constexpr int WARP_LEAVES = 64;  // leaf slots per warp for long pairwise segments
+constexpr int THREAD_LANE_ROW = 32;   // lane-tree rows up to this: one thread per row
+constexpr int THREAD_PW_ROW = 128;    // pairwise rows up to this: one thread per row
+constexpr int MED_ROW = 1024;         // longer rows of a tile: one warp per row, from shared
+                                      // memory (rows above MED_ROW: one CTA each, cta_long_row)
+constexpr int MED_LEAVES = 16;        // pairwise leaves of a <= 1024-entry segment (max 9)
 
 // LibB: p[s] + pairwise(p[s+1:e]); LibC: the row cut at the chunk bounds,
 // each piece reduced that way and added from 0 in chunk order.
-template <class T, class G>
-__device__ __forceinline__ T pw_row_value(const G& get, int64_t s, int64_t e, const int64_t* __restrict__ bounds,
-                                          int nb) {
-  if (bounds == nullptr) return e == s ? T(0) : segment_sum<T>(get, s, e);
+__device__ __forceinline__ int first_bound_after(const int64_t* __restrict__ bounds, int nb, int64_t s) {
   int lo = 0, hi = nb;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (bounds[mid] <= s) lo = mid + 1; else hi = mid;
   }
+  return lo;
+}
+
+template <class T, class G>
+__device__ __forceinline__ T pw_row_value(const G& get, int64_t s, int64_t e, const int64_t* __restrict__ bounds,
+                                          int nb) {
+  if (bounds == nullptr) return e == s ? T(0) : segment_sum<T>(get, s, e);
   T acc = T(0);
-  for (int64_t cur = s; cur < e; ++lo) {
+  for (int64_t cur = s, lo = first_bound_after(bounds, nb, s); cur < e; ++lo) {
     const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
     acc = acc + segment_sum<T>(get, cur, nxt);
     cur = nxt;
@@ -88,49 +112,43 @@ __device__ __forceinline__ T pw_row_value(const G& get, int64_t s, int64_t e, co
   return acc;
 }
 
-// Warp-cooperative p[s] + pairwise(p[s+1:e]) for one long segment: lane 0
-// enumerates the recursion's leaves, 8 lanes evaluate each leaf (one lane
-// per numpy accumulator, combined with the same ((r0+r1)+(r2+r3))+... tree),
-// then lane 0 combines the leaf sums along the recursion.  Result on lane 0.
-template <class T, class G>
-__device__ T warp_pw_segment(const G& get, int64_t s, int64_t e, int64_t* loff, int* llen, T* lsum) {
+// Warp-cooperative pairwise(p[lo : lo+n]) for a subtree of at most CAP
+// leaves: lane 0 enumerates the recursion's leaves, 8 lanes evaluate each
+// leaf (one lane per numpy accumulator, combined with the same
+// ((r0+r1)+(r2+r3))+... tree), then lane 0 combines the leaf sums along the
+// recursion.  Called by the whole (converged) warp; result on every lane.
+template <int CAP, class T, class G>
+__device__ T warp_pw_block(const G& get, int64_t lo, int64_t n, int64_t* loff, int* llen, T* lsum) {
   const int lane = threadIdx.x & 31;
-  const int64_t m = e - s - 1;  // elements of the pairwise part
-  if (m <= 0) return get(s);
   int nleaf = 0;
   if (lane == 0) {
-    pw_traverse<T>([&](int64_t lo, int64_t n) {
-      if (nleaf < WARP_LEAVES) {
-        loff[nleaf] = lo;
-        llen[nleaf] = (int)n;
+    pw_traverse<T>([&](int64_t l, int64_t m) {
+      if (nleaf < CAP) {
+        loff[nleaf] = l;
+        llen[nleaf] = (int)m;
       }
       ++nleaf;
       return T(0);
-    }, s + 1, m);
+    }, lo, n);
   }
   nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
-  if (nleaf > WARP_LEAVES) {  // extremely long segment: sequential fallback
-    T r = T(0);
-    if (lane == 0) r = segment_sum<T>(get, s, e);
-    return r;
-  }
   __syncwarp();
   const int grp = lane >> 3, k = lane & 7;
   for (int l0 = 0; l0 < nleaf; l0 += 4) {
     const int li = l0 + grp;
     T r = T(0);
-    int64_t lo = 0;
-    int n = 0;
+    int64_t b = 0;
+    int m = 0;
     if (li < nleaf) {
-      lo = loff[li];
-      n = llen[li];
+      b = loff[li];
+      m = llen[li];
     }
-    if (n >= 8) {
-      r = get(lo + k);
-      const int lim = n - (n % 8);
-      for (int i = 8; i < lim; i += 8) r = r + get(lo + i + k);
+    if (m >= 8) {
+      r = get(b + k);
+      const int lim = m - (m % 8);
+#pragma unroll 4
+      for (int i = 8; i < lim; i += 8) r = r + get(b + i + k);
     }
-    // fixed combine tree inside each 8-lane group
     T o = __shfl_down_sync(0xffffffffu, r, 1);
     if ((k & 1) == 0) r = r + o;
     o = __shfl_down_sync(0xffffffffu, r, 2);
@@ -138,12 +156,12 @@ __device__ T warp_pw_segment(const G& get, int64_t s, int64_t e, int64_t* loff, 
     o = __shfl_down_sync(0xffffffffu, r, 4);
     if (k == 0) r = r + o;
     if (k == 0 && li < nleaf) {
-      if (n < 8) {
+      if (m < 8) {
         T q = T(-0.0);
-        for (int i = 0; i < n; ++i) q = q + get(lo + i);
+        for (int i = 0; i < m; ++i) q = q + get(b + i);
         r = q;
       } else {
-        for (int i = n - (n % 8); i < n; ++i) r = r + get(lo + i);
+        for (int i = m - (m % 8); i < m; ++i) r = r + get(b + i);
       }
       lsum[li] = r;
     }
@@ -152,137 +170,445 @@ __device__ T warp_pw_segment(const G& get, int64_t s, int64_t e, int64_t* loff, 
   T total = T(0);
   if (lane == 0) {
     int next = 0;
-    total = pw_traverse<T>([&](int64_t, int64_t) { return lsum[next++]; }, s + 1, m);
-    total = get(s) + total;
+    total = pw_traverse<T>([&](int64_t, int64_t) { return lsum[next++]; }, lo, n);
   }
+  total = __shfl_sync(0xffffffffu, total, 0);
+  __syncwarp();  // the leaf slots are reused by the next call
   return total;
 }
 
-// Warp-cooperative L-lane CSR-vector row (len > LONG_ROW >= L): lane t < L
-// sums elements t, t+L, ... in order; halving tree.  Result on lane 0.
-template <class T, class G>
-__device__ T warp_lane_row(const G& get, int64_t s, int64_t len, int L) {
-  const int lane = threadIdx.x & 31;
+// p[s] + pairwise(p[s+1:e]) by one warp: the top of the recursion is walked
+// by every lane in step, subtrees of at most `span` entries (<= CAP leaves)
+// are reduced leaf-parallel.  Result on every lane.
+template <int CAP, class T, class G>
+__device__ T warp_pw_segment(const G& get, int64_t s, int64_t e, int64_t* loff, int* llen, T* lsum) {
+  const int64_t m = e - s - 1;
+  if (m <= 0) return get(s);
+  constexpr int64_t span = CAP >= 33 ? 4096 : CAP >= 17 ? 2048 : CAP >= 9 ? 1024 : 512;
+  const T tail = pw_traverse<T>(
+      [&](int64_t lo, int64_t n) { return warp_pw_block<CAP, T>(get, lo, n, loff, llen, lsum); }, s + 1, m, span);
+  return get(s) + tail;
+}
+
+// LibB / LibC row by one warp (see pw_row_value).  Result on every lane.
+template <int CAP, class T, class G>
+__device__ T warp_pw_row(const G& get, int64_t s, int64_t e, const int64_t* __restrict__ bounds, int nb,
+                         int64_t* loff, int* llen, T* lsum) {
+  if (bounds == nullptr) return e == s ? T(0) : warp_pw_segment<CAP, T>(get, s, e, loff, llen, lsum);
   T acc = T(0);
-  if (lane < L)
-    for (int64_t k = lane; k < len; k += L) acc = acc + get(s + k);
-  for (int h = L >> 1; h >= 1; h >>= 1) {
-    const T o = __shfl_down_sync(0xffffffffu, acc, h);
-    if (lane < h) acc = acc + o;
+  for (int64_t cur = s, lo = first_bound_after(bounds, nb, s); cur < e; ++lo) {
+    const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
+    acc = acc + warp_pw_segment<CAP, T>(get, cur, nxt, loff, llen, lsum);
+    cur = nxt;
   }
   return acc;
 }
 
-// ---------------------------------------------------------------------------
-// CSR/LibA/L (kernels.py:167-189), CSR/LibB (kernels.py:192-199) and
-// CSR/LibC (kernels.py:202-223).  Each CTA owns 128 consecutive rows; all
-// threads stage the rows' products p = v*x[c] in shared memory with
-// coalesced loads and U independent gathers in flight per thread; then one
-// thread per row reduces it in the configuration's exact order (lane tree,
-// numpy pairwise, or chunk pieces) and rows longer than LONG_ROW are reduced
-// by a whole warp (leaf-parallel pairwise / L lanes).  CTAs whose entries
-// exceed the staging capacity read their products from global memory.
-// ---------------------------------------------------------------------------
-template <class T, class P, bool ADD>
-__global__ void __launch_bounds__(ROWSEG_ROWS) k_csr_rowseg(int64_t nrows, const P* __restrict__ ptr,
-                                                            const int* __restrict__ cols,
-                                                            const T* __restrict__ vals,
-                                                            const T* __restrict__ x, T* __restrict__ y,
-                                                            const int64_t* __restrict__ bounds, int nb,
-                                                            int lanes) {
-  __shared__ int64_t sptr[ROWSEG_ROWS + 1];
-  __shared__ T sp[ROWSEG_CAP];
-  const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * ROWSEG_ROWS;
-  const int nr = (int)(nrows - r0 < ROWSEG_ROWS ? nrows - r0 : ROWSEG_ROWS);
-  for (int i = tid; i <= nr; i += blockDim.x) sptr[i] = ptr[r0 + i];
-  __syncthreads();
-  const int64_t E0 = sptr[0];
-  // stage the CTA's products (a prefix when long rows push it past capacity)
-  const int64_t E1 = sptr[nr] - E0 <= ROWSEG_CAP ? sptr[nr] : E0 + ROWSEG_CAP;
-  {
-    constexpr int U = 4;
-    for (int64_t k = E0 + tid; k < E1; k += (int64_t)ROWSEG_ROWS * U) {
-      T v[U];
-      int c[U];
+// Warp-cooperative L-lane CSR-vector row: lane t < L sums elements t, t+L,
+// ... in order, then the halving tree.  The whole warp loads the row in
+// coalesced chunks of 4x32 products (all in flight at once); lane t < L then
+// takes its elements of each 32-chunk by shuffle (element j of a chunk
+// belongs to leaf j % L because L divides 32).  Past-the-end elements are
+// +0.0 and leave the (never -0.0) partial sums unchanged.  Result on every
+// lane.
+template <class T, class G>
+__device__ T warp_lane_row(const G& get, int64_t s, int64_t len, int L) {
+  const int lane = threadIdx.x & 31;
+  T acc = T(0);
+  for (int64_t base = 0; base < len; base += 128) {
+    T p[4];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t kk = k + (int64_t)u * ROWSEG_ROWS;
-        if (kk < E1) {
-          v[u] = ld_stream(vals + kk);
-          c[u] = ld_stream(cols + kk);
+    for (int c = 0; c < 4; ++c) {
+      const int64_t k = base + c * 32 + lane;
+      p[c] = k < len ? get(s + k) : T(0);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (L == 32) {
+        acc = acc + p[c];
+      } else {
+        for (int j = 0; j < 32; j += L) {
+          const T q = __shfl_sync(0xffffffffu, p[c], j + (lane & (L - 1)));
+          if (lane < L) acc = acc + q;
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t kk = k + (int64_t)u * ROWSEG_ROWS;
-        if (kk < E1) sp[kk - E0] = v[u] * ld_x(x + c[u]);
-      }
-    }
-    __syncthreads();
-  }
-  auto get_s = [&](int64_t k) { return sp[k - E0]; };
-  auto get_g = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
-  if (tid < nr) {
-    const int64_t s = sptr[tid], e = sptr[tid + 1];
-    if (e - s <= (lanes > 0 ? LONG_LANE_ROW : LONG_ROW)) {
-      const bool staged = e <= E1;
-      T v;
-      if (lanes > 0) v = staged ? lane_tree_sum<T>(get_s, s, e - s, lanes) : lane_tree_sum<T>(get_g, s, e - s, lanes);
-      else v = staged ? pw_row_value<T>(get_s, s, e, bounds, nb) : pw_row_value<T>(get_g, s, e, bounds, nb);
-      if (!ADD) y[r0 + tid] = v;
-      else if (e > s) y[r0 + tid] = y[r0 + tid] + v;   // HYB spill: rows with entries only
     }
   }
-  // rows longer than LONG_ROW are reduced by k_long_rows
+  for (int h = L >> 1; h >= 1; h >>= 1) {
+    const T o = __shfl_down_sync(0xffffffffu, acc, h);
+    if (lane < h) acc = acc + o;
+  }
+  return __shfl_sync(0xffffffffu, acc, 0);
 }
+
 // ---------------------------------------------------------------------------
-// Long rows / runs (> LONG_ROW entries) of any row-sorted layout: one warp
-// per segment from a per-handle list, so the few heavy rows of a power-law
-// matrix run side by side instead of serialising inside one CTA.  Exact
-// order as the thread path (lane tree / pairwise / chunk pieces).
+// Row kernel for every row-sorted layout: CSR/LibA/L (kernels.py:167-189),
+// CSR/LibB (kernels.py:192-199), CSR/LibC (kernels.py:202-223), COO/LibA
+// over the cached run starts (kernels.py:141-153) and the HYB spill
+// (kernels.py:262-270, ADD).
+//
+// The rows are cut once per handle into tiles (RowTile: at most ROWSEG_ROWS
+// rows and CAP entries, rows longer than MED_ROW excluded — those are reduced
+// first, one CTA each, by cta_long_row).  A persistent CTA (one wave) walks
+// its tiles through an NS-deep shared-memory ring:
+//   * one thread arms the stage's mbarrier and the TMA engine bulk-copies the
+//     tile's row-pointer slice and its vals/cols (16-B aligned supersets,
+//     L2 evict-first) into the stage — NS-1 tiles are in flight while one is
+//     reduced;
+//   * the x gathers of the next tile are issued into registers before the
+//     current tile is reduced, and multiplied in place afterwards;
+//   * one thread per row reduces it in the configuration's exact order
+//     (lane tree / numpy pairwise / chunk pieces); rows longer than the
+//     thread limit are reduced by a warp from shared memory.
 // ---------------------------------------------------------------------------
-template <class T, bool ADD>
-__global__ void __launch_bounds__(128) k_long_rows(int64_t nlong, const int* __restrict__ lrow,
-                                                   const int64_t* __restrict__ lbeg, const int64_t* __restrict__ lend,
-                                                   const int* __restrict__ cols, const T* __restrict__ vals,
-                                                   const T* __restrict__ x, T* __restrict__ y,
-                                                   const int64_t* __restrict__ bounds, int nb, int lanes) {
-  __shared__ int64_t loff[4][WARP_LEAVES];
-  __shared__ int llen[4][WARP_LEAVES];
-  __shared__ T lsum[4][WARP_LEAVES];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto get = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
-  for (int64_t i = (int64_t)blockIdx.x * 4 + warp; i < nlong; i += (int64_t)gridDim.x * 4) {
-    const int64_t s = lbeg[i], e = lend[i];
-    if (lanes == 0 && e - s <= LONG_ROW) continue;   // done by the thread path
-    T v;
-    if (lanes > 0) {
-      v = warp_lane_row<T>(get, s, e - s, lanes);
-    } else if (bounds == nullptr) {
-      v = warp_pw_segment<T>(get, s, e, loff[warp], llen[warp], lsum[warp]);
-    } else {
-      int lo = 0, hi = nb;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (bounds[mid] <= s) lo = mid + 1; else hi = mid;
+struct RowTile {
+  long long e0, e1;  // entry range [e0, e1)
+  int r0, r1;        // row range [r0, r1)
+};
+// Stage layout of the ring: vals (products in place), cols, row-pointer slice.
+template <class T, class P, int CAP, int NS>
+struct PipeLayout {
+  static constexpr int PQ = 16 / (int)sizeof(P);  // row-pointer entries per 16 B
+  static constexpr size_t SV = (size_t)(CAP + 8) * sizeof(T);
+  static constexpr size_t SC = (size_t)(CAP + 8) * 4;
+  static constexpr size_t SP = ((size_t)(ROWSEG_ROWS + 1 + 2 * PQ) * sizeof(P) + 15) / 16 * 16;
+  static constexpr size_t STAGE = (SV + SC + SP + 127) / 128 * 128;
+  static constexpr size_t BYTES = NS * STAGE;
+};
+
+template <class T, class P, class L>
+__device__ __forceinline__ void issue_tile(unsigned char* stage, uint64_t* bar, const RowTile& t,
+                                           const P* __restrict__ ptr, const int* __restrict__ cols,
+                                           const T* __restrict__ vals, uint64_t policy) {
+  const int64_t pa = t.r0 & ~(int64_t)(L::PQ - 1);
+  const int64_t pb = ((int64_t)t.r1 + 1 + L::PQ - 1) & ~(int64_t)(L::PQ - 1);
+  const uint32_t np = (uint32_t)((pb - pa) * sizeof(P));
+  uint32_t nv = 0, nc = 0;
+  int64_t A0 = 0;
+  if (t.e1 > t.e0) {
+    A0 = t.e0 & ~int64_t(3);
+    const int64_t A1 = (t.e1 + 3) & ~int64_t(3);
+    nv = (uint32_t)((A1 - A0) * sizeof(T));
+    nc = (uint32_t)((A1 - A0) * 4);
+  }
+  mbar_expect_tx(bar, np + nv + nc);
+  bulk_g2s(stage + L::SV + L::SC, ptr + pa, np, bar);
+  if (nv) {
+    bulk_g2s_hint(stage, vals + A0, nv, bar, policy);
+    bulk_g2s_hint(stage + L::SV, cols + A0, nc, bar, policy);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Rows longer than MED_ROW (a per-handle list): one whole CTA per row, before
+// the CTA starts its tiles.  The row's products are staged through the (not
+// yet used) ring in chunks of LONG_CHUNK with coalesced loads, all in flight,
+// then reduced from shared memory in the configuration's exact order:
+//   lane tree  - thread t < L runs leaf t over the chunk (chunk starts are
+//                multiples of 32, so leaf membership is k % L), then the
+//                halving tree in warp 0;
+//   pairwise   - the recursion's top is walked by every thread in step; each
+//                subtree of <= LONG_CHUNK addends is staged, its leaves are
+//                evaluated by 8-thread groups (one per numpy accumulator),
+//                thread 0 combines them along the recursion.
+// ---------------------------------------------------------------------------
+constexpr int LONG_CHUNK = 2048;
+constexpr int LONG_CHUNK_LEAVES = 24;  // leaves of a <= 2048-addend subtree (max 17)
+
+struct LongScratch {
+  int64_t loff[LONG_CHUNK_LEAVES];
+  int llen[LONG_CHUNK_LEAVES];
+  double lsum[LONG_CHUNK_LEAVES];
+  double bcast;
+  int nleaf;
+};
+
+template <class T>
+__device__ __forceinline__ void stage_products(T* buf, int64_t lo, int n, const int* __restrict__ cols,
+                                               const T* __restrict__ vals, const T* __restrict__ x) {
+  constexpr int U = 8;
+  for (int i = threadIdx.x; i < n; i += ROWSEG_ROWS * U) {
+    T v[U];
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = i + u * ROWSEG_ROWS;
+      if (j < n) {
+        v[u] = ld_stream(vals + lo + j);
+        c[u] = ld_stream(cols + lo + j);
       }
-      T acc = T(0);
-      for (int64_t cur = s; cur < e; ++lo) {
-        const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
-        const T piece = warp_pw_segment<T>(get, cur, nxt, loff[warp], llen[warp], lsum[warp]);
-        acc = acc + piece;
-        cur = nxt;
-      }
-      v = acc;
     }
-    if (lane == 0) {
-      if (ADD) y[lrow[i]] = y[lrow[i]] + v;
-      else y[lrow[i]] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = i + u * ROWSEG_ROWS;
+      if (j < n) buf[j] = v[u] * ld_x(x + c[u]);
     }
   }
 }
 
+// pairwise(p[lo : lo+n]), n <= LONG_CHUNK, by the whole CTA; result on all threads
+template <class T>
+__device__ T cta_pw_block(T* buf, LongScratch* sc, int64_t lo, int64_t n, const int* __restrict__ cols,
+                          const T* __restrict__ vals, const T* __restrict__ x) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  stage_products<T>(buf, lo, (int)n, cols, vals, x);
+  if (tid == 0) {
+    int nl = 0;
+    pw_traverse<T>([&](int64_t l, int64_t m) {
+      sc->loff[nl] = l - lo;
+      sc->llen[nl] = (int)m;
+      ++nl;
+      return T(0);
+    }, lo, n);
+    sc->nleaf = nl;
+  }
+  __syncthreads();
+  const int nleaf = sc->nleaf;
+  const int grp = lane >> 3, k = lane & 7;
+  for (int l0 = warp * 4; l0 < nleaf; l0 += ROWSEG_ROWS / 8) {
+    const int li = l0 + grp;
+    int b = 0, m = 0;
+    if (li < nleaf) {
+      b = (int)sc->loff[li];
+      m = sc->llen[li];
+    }
+    T r = T(0);
+    if (m >= 8) {
+      r = buf[b + k];
+      const int lim = m - (m % 8);
+      for (int i = 8; i < lim; i += 8) r = r + buf[b + i + k];
+    }
+    T o = __shfl_down_sync(0xffffffffu, r, 1);
+    if ((k & 1) == 0) r = r + o;
+    o = __shfl_down_sync(0xffffffffu, r, 2);
+    if ((k & 3) == 0) r = r + o;
+    o = __shfl_down_sync(0xffffffffu, r, 4);
+    if (k == 0) r = r + o;
+    if (k == 0 && li < nleaf) {
+      if (m < 8) {
+        T q = T(-0.0);
+        for (int i = 0; i < m; ++i) q = q + buf[b + i];
+        r = q;
+      } else {
+        for (int i = m - (m % 8); i < m; ++i) r = r + buf[b + i];
+      }
+      sc->lsum[li] = (double)r;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int next = 0;
+    sc->bcast = (double)pw_traverse<T>([&](int64_t, int64_t) { return (T)sc->lsum[next++]; }, lo, n);
+  }
+  __syncthreads();
+  const T res = (T)sc->bcast;
+  __syncthreads();  // buf and the scratch are reused by the next block
+  return res;
+}
+
+template <class T, bool ADD, bool LANE>
+__device__ void cta_long_row(int row, int64_t s, int64_t e, const int* __restrict__ cols, const T* __restrict__ vals,
+                             const T* __restrict__ x, T* __restrict__ y, const int64_t* __restrict__ bounds, int nb,
+                             int lanes, T* buf, LongScratch* sc) {
+  const int tid = threadIdx.x;
+  T v;
+  if constexpr (LANE) {
+    T acc = T(0);
+    for (int64_t base = s; base < e; base += LONG_CHUNK) {
+      const int n = (int)(e - base < LONG_CHUNK ? e - base : LONG_CHUNK);
+      stage_products<T>(buf, base, n, cols, vals, x);
+      __syncthreads();
+      if (tid < lanes)
+        for (int k = tid; k < n; k += lanes) acc = acc + buf[k];
+      __syncthreads();
+    }
+    if (tid < 32)
+      for (int h = lanes >> 1; h >= 1; h >>= 1) {
+        const T o = __shfl_down_sync(0xffffffffu, acc, h);
+        if (tid < h) acc = acc + o;
+      }
+    v = acc;
+  } else {
+    auto get_g = [&](int64_t k) { return ld_stream(vals + k) * ld_x(x + ld_stream(cols + k)); };
+    auto segment = [&](int64_t a, int64_t b) {
+      const int64_t m = b - a - 1;
+      if (m <= 0) return get_g(a);
+      const T tail = pw_traverse<T>(
+          [&](int64_t lo, int64_t n) { return cta_pw_block<T>(buf, sc, lo, n, cols, vals, x); }, a + 1, m,
+          LONG_CHUNK);
+      return get_g(a) + tail;
+    };
+    if (bounds == nullptr) {
+      v = segment(s, e);
+    } else {
+      T acc = T(0);
+      for (int64_t cur = s, lo = first_bound_after(bounds, nb, s); cur < e; ++lo) {
+        const int64_t nxt = (lo < nb && bounds[lo] < e) ? bounds[lo] : e;
+        acc = acc + segment(cur, nxt);
+        cur = nxt;
+      }
+      v = acc;
+    }
+  }
+  if (tid == 0) {
+    if (ADD) y[row] = y[row] + v;
+    else y[row] = v;
+  }
+}
+
+// LANE: CSR/LibA/L lane tree; otherwise numpy pairwise (LibB, COO/LibA, HYB
+// spill) or chunk pieces (LibC, bounds != nullptr).
+template <class T, class P, bool ADD, bool LANE, int CAP, int NS>
+__global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, const RowTile* __restrict__ tiles,
+                                                           const P* __restrict__ ptr, const int* __restrict__ cols,
+                                                           const T* __restrict__ vals, const T* __restrict__ x,
+                                                           T* __restrict__ y, const int64_t* __restrict__ bounds,
+                                                           int nb, int lanes, int64_t nlong,
+                                                           const int* __restrict__ lrow,
+                                                           const int64_t* __restrict__ lbeg,
+                                                           const int64_t* __restrict__ lend) {
+  using L = PipeLayout<T, P, CAP, NS>;
+  constexpr int U = CAP / ROWSEG_ROWS;  // products per thread per tile (one round of gathers)
+  static_assert(CAP % ROWSEG_ROWS == 0 && CAP >= MED_ROW, "tile capacity");
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ alignas(8) uint64_t bar[NS];
+  __shared__ RowTile desc[NS];
+  __shared__ int smed[ROWSEG_ROWS];
+  __shared__ int nmed;
+  constexpr int NL = LANE ? 1 : MED_LEAVES;
+  __shared__ int64_t loff[ROWSEG_ROWS / 32][NL];
+  __shared__ int llen[ROWSEG_ROWS / 32][NL];
+  __shared__ T lsum[ROWSEG_ROWS / 32][NL];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int thr = LANE ? THREAD_LANE_ROW : THREAD_PW_ROW;
+  const uint64_t policy = l2_evict_first_policy();
+  if (nlong > 0) {
+    static_assert(L::BYTES >= LONG_CHUNK * sizeof(T) + sizeof(LongScratch), "ring too small for long rows");
+    T* buf = reinterpret_cast<T*>(ring);
+    LongScratch* lsc = reinterpret_cast<LongScratch*>(ring + LONG_CHUNK * sizeof(T));
+    for (int64_t li = blockIdx.x; li < nlong; li += gridDim.x) {
+      cta_long_row<T, ADD, LANE>(lrow[li], lbeg[li], lend[li], cols, vals, x, y, bounds, nb, lanes, buf, lsc);
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      const int64_t ti = blockIdx.x + (int64_t)s * gridDim.x;
+      if (ti < ntiles) {
+        desc[s] = tiles[ti];
+        issue_tile<T, P, L>(ring + s * L::STAGE, &bar[s], desc[s], ptr, cols, vals, policy);
+      }
+    }
+  }
+  __syncthreads();
+  // The x gathers of tile i+1 are issued before tile i is reduced, so their
+  // latency hides behind the reduction (software pipelining in registers).
+  T xv[U];
+  int gather_it = 0;
+  auto gather = [&](int st) {
+    const RowTile& g = desc[st];
+    const int gn = (int)(g.e1 - g.e0), goff = (int)(g.e0 - (g.e0 & ~int64_t(3)));
+    const int* gsc = reinterpret_cast<const int*>(ring + st * L::STAGE + L::SV);
+    mbar_wait(&bar[st], (uint32_t)(gather_it / NS) & 1u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = tid + u * ROWSEG_ROWS;
+      if (j < gn) xv[u] = ld_x(x + gsc[goff + j]);
+    }
+  };
+  if (blockIdx.x < ntiles) gather(0);
+  int it = 0;
+  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+    const int st = it % NS;
+    unsigned char* stage = ring + st * L::STAGE;
+    T* sv = reinterpret_cast<T*>(stage);
+    const P* sp = reinterpret_cast<const P*>(stage + L::SV + L::SC);
+    // descriptor of the tile this stage takes next, fetched early
+    const int64_t tn = ti + (int64_t)NS * gridDim.x;
+    RowTile nxt{};
+    if (tid == 0 && tn < ntiles) nxt = tiles[tn];
+    const RowTile t = desc[st];
+    const int64_t pa = t.r0 & ~(int64_t)(L::PQ - 1);
+    const int64_t A0 = t.e0 & ~int64_t(3);
+    const int n = (int)(t.e1 - t.e0), off = (int)(t.e0 - A0);
+    if (tid == 0) nmed = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = tid + u * ROWSEG_ROWS;
+      if (j < n) sv[off + j] = sv[off + j] * xv[u];
+    }
+    __syncthreads();
+    if (ti + gridDim.x < ntiles) {
+      gather_it = it + 1;
+      gather((it + 1) % NS);
+    }
+    auto get_s = [&](int64_t k) { return sv[(int)(k - A0)]; };
+    const int nr = t.r1 - t.r0;
+    const bool mine = tid < nr;
+    const int64_t s = mine ? (int64_t)sp[t.r0 + tid - pa] : 0;
+    const int64_t e = mine ? (int64_t)sp[t.r0 + tid + 1 - pa] : 0;
+    const int len = (int)(e - s);
+    const bool thread_row = mine && len <= thr;
+    if (mine && !thread_row) smed[atomicAdd(&nmed, 1)] = tid;
+    T v = T(0);
+    if constexpr (LANE) {
+      const int wmax = __reduce_max_sync(0xffffffffu, thread_row ? len : 0);
+      const int base = (int)(s - A0);
+      if (thread_row) v = lane_tree_warp<T>([&](int k) { return sv[base + k]; }, len, lanes, wmax);
+    } else {
+      if (thread_row) v = pw_row_value<T>(get_s, s, e, bounds, nb);
+    }
+    const int64_t row = (int64_t)t.r0 + tid;
+    if (thread_row) {
+      if (!ADD) y[row] = v;
+      else if (len > 0) y[row] = y[row] + v;   // HYB spill: rows with entries only
+    }
+    __syncthreads();
+    for (int i = warp; i < nmed; i += ROWSEG_ROWS / 32) {
+      const int rr = smed[i];
+      const int64_t s2 = sp[t.r0 + rr - pa], e2 = sp[t.r0 + rr + 1 - pa];
+      T w;
+      if constexpr (LANE) w = warp_lane_row<T>(get_s, s2, e2 - s2, lanes);
+      else w = warp_pw_row<MED_LEAVES, T>(get_s, s2, e2, bounds, nb, loff[warp], llen[warp], lsum[warp]);
+      if (lane == 0) {
+        if (!ADD) y[(int64_t)t.r0 + rr] = w;
+        else y[(int64_t)t.r0 + rr] = y[(int64_t)t.r0 + rr] + w;
+      }
+    }
+    __syncthreads();  // stage st and the medium-row list are free again
+    if (tid == 0 && tn < ntiles) {
+      fence_proxy_async_smem();
+      desc[st] = nxt;
+      issue_tile<T, P, L>(stage, &bar[st], nxt, ptr, cols, vals, policy);
+    }
+  }
+}
+
+// Tiles of a row pointer: each 128-row block is cut greedily into runs of
+// rows of at most `cap` entries, skipping rows longer than MED_ROW.  Pass 1
+// (out == nullptr) counts per block, pass 2 writes at the scanned offsets.
+template <class P>
+__global__ void k_make_tiles(int64_t nrows, const P* __restrict__ ptr, int64_t cap, int64_t* __restrict__ counts,
+                             const int64_t* __restrict__ offs, RowTile* __restrict__ out) {
+  const int64_t nblk = (nrows + ROWSEG_ROWS - 1) / ROWSEG_ROWS;
+  for (int64_t blk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; blk < nblk;
+       blk += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = blk * ROWSEG_ROWS, end = b0 + ROWSEG_ROWS < nrows ? b0 + ROWSEG_ROWS : nrows;
+    int64_t cnt = 0, a = b0;
+    while (true) {
+      while (a < end && (int64_t)ptr[a + 1] - (int64_t)ptr[a] > MED_ROW) ++a;
+      if (a >= end) break;
+      const int64_t ea = ptr[a];
+      int64_t b = a;
+      while (b < end && (int64_t)ptr[b + 1] - (int64_t)ptr[b] <= MED_ROW && (int64_t)ptr[b + 1] - ea <= cap) ++b;
+      if (out) out[offs[blk] + cnt] = RowTile{ea, (long long)ptr[b], (int)a, (int)b};
+      ++cnt;
+      a = b;
+    }
+    if (!out) counts[blk] = cnt;
+  }
+}
 // ---------------------------------------------------------------------------
 // COO/LibB (kernels.py:156-164): scatter-accumulate with fp64 atomics.  Runs
 // of equal rows inside a warp are pre-summed with a segmented shuffle scan so
@@ -494,13 +820,13 @@ static const long long* coo_runs(const svb_matrix* m, cudaStream_t s) {
   return ptr<long long>(m->dptr);
 }
 
-// rows of a row pointer longer than LONG_LANE_ROW -> (row, begin, end) list
+// rows of a row pointer longer than MED_ROW -> (row, begin, end) list
 template <class P>
 __global__ void k_find_long(int64_t nrows, const P* __restrict__ ptr, unsigned long long* count, int* lrow,
                             int64_t* lbeg, int64_t* lend) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = ptr[i], e = ptr[i + 1];
-    if (e - b > LONG_LANE_ROW) {
+    if (e - b > MED_ROW) {
       const unsigned long long k = atomicAdd(count, 1ull);
       lrow[k] = (int)i;
       lbeg[k] = b;
@@ -515,7 +841,7 @@ static int64_t long_list(const svb_matrix* m, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(m->mu);
   if (m->nlong >= 0) return m->nlong;
   const int64_t entries = m->fmt == SVB_HYB ? m->spill_nnz : m->nnz;
-  const int64_t cap = entries / (LONG_LANE_ROW + 1) + 1;
+  const int64_t cap = entries / (MED_ROW + 1) + 1;
   m->lrow = alloc(cap * 4, s);
   m->lbeg = alloc(cap * 8, s);
   m->lend = alloc(cap * 8, s);
@@ -545,21 +871,89 @@ static int64_t long_list(const svb_matrix* m, cudaStream_t s) {
   return m->nlong;
 }
 
-template <class T, bool ADD>
-static void launch_long(const svb_matrix* m, const int* cols, const T* vals, const T* x, T* y,
-                        const int64_t* bounds, int nb, int lanes, cudaStream_t s) {
-  const int64_t nl = long_list(m, s);
-  if (nl <= 0) return;
-  const unsigned g = (unsigned)((nl + 3) / 4);
-  k_long_rows<T, ADD><<<g, 128, 0, s>>>(nl, ptr<int>(m->lrow), ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend),
-                                        cols, vals, x, y, bounds, nb, lanes);
+// The handle's row tiles (built once per capacity, cached) over its row
+// pointer: CSR rows, COO runs (derived pointer) or the HYB spill rows.
+template <class P>
+static int64_t tile_list(const svb_matrix* m, const P* rp, int cap, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->ntiles >= 0 && m->tile_cap == cap) return m->ntiles;
+  const int64_t nblk = (m->nrows + ROWSEG_ROWS - 1) / ROWSEG_ROWS;
+  Buf cnt = alloc((nblk + 1) * 8, s), off = alloc((nblk + 1) * 8, s);
+  const unsigned g = grid_for(nblk, 128);
+  k_make_tiles<P><<<g, 128, 0, s>>>(m->nrows, rp, cap, ptr<int64_t>(cnt), nullptr, nullptr);
   SVB_CHECK_LAUNCH();
+  const int64_t total = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(off), nblk, s);
+  Buf tiles = alloc((total > 0 ? total : 1) * sizeof(RowTile), s);
+  if (total > 0) {
+    k_make_tiles<P><<<g, 128, 0, s>>>(m->nrows, rp, cap, nullptr, ptr<int64_t>(off), ptr<RowTile>(tiles));
+    SVB_CHECK_LAUNCH();
+  }
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));  // an older tile list may still be in use elsewhere
+  detach(tiles);
+  m->tiles = tiles;
+  m->tile_cap = cap;
+  m->ntiles = total;
+  return total;
+}
+
+template <class T, class P, bool ADD, bool LANE, int CAP, int NS>
+static void launch_rows_cfg(const svb_matrix* m, const P* rp, const int* cols, const T* vals, const T* x, T* y,
+                            const int64_t* bounds, int nb, int lanes, cudaStream_t s) {
+  using L = PipeLayout<T, P, CAP, NS>;
+  const int64_t nt = tile_list(m, rp, CAP, s);
+  const int64_t nl = long_list(m, s);
+  const int64_t work = nt > nl ? nt : nl;
+  if (work <= 0) return;
+  static const int occ = [] {
+    SVB_CUDA_TRY(cudaFuncSetAttribute(k_rows_pipe<T, P, ADD, LANE, CAP, NS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES));
+    int o = 0;
+    SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_rows_pipe<T, P, ADD, LANE, CAP, NS>,
+                                                               ROWSEG_ROWS, L::BYTES));
+    return o < 1 ? 1 : o;
+  }();
+  const int64_t cap = (int64_t)sm_count() * occ;
+  const unsigned g = (unsigned)(work < cap ? work : cap);
+  k_rows_pipe<T, P, ADD, LANE, CAP, NS><<<g, ROWSEG_ROWS, L::BYTES, s>>>(
+      nt, ptr<RowTile>(m->tiles), rp, cols, vals, x, y, bounds, nb, lanes, nl, ptr<int>(m->lrow),
+      ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend));
+  SVB_CHECK_LAUNCH();
+}
+
+// The persistent row kernel.  The tile capacity follows the mean entries per
+// 128-row block (a full stage wastes least ring space); SPMVTUNE_ROWCFG=1..3
+// pins a variant for experiments.
+template <class T, class P, bool ADD>
+static void launch_rows(const svb_matrix* m, const P* rp, const int* cols, const T* vals, const T* x, T* y,
+                        const int64_t* bounds, int nb, int lanes, cudaStream_t s) {
+  static const int forced = [] {
+    const char* e = getenv("SPMVTUNE_ROWCFG");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t entries = m->fmt == SVB_HYB ? m->spill_nnz : m->nnz;
+  const double per_block = m->nrows ? (double)entries * ROWSEG_ROWS / (double)m->nrows : 0.0;
+  const int cfg = forced ? forced : per_block <= 900 ? 3 : per_block <= 1400 ? 1 : 2;
+  auto go = [&](auto lane_tag) {
+    constexpr bool LANE = decltype(lane_tag)::value;
+    switch (cfg) {
+      case 3: launch_rows_cfg<T, P, ADD, LANE, 1024, 3>(m, rp, cols, vals, x, y, bounds, nb, lanes, s); break;
+      case 1: launch_rows_cfg<T, P, ADD, LANE, 1536, 2>(m, rp, cols, vals, x, y, bounds, nb, lanes, s); break;
+      default: launch_rows_cfg<T, P, ADD, LANE, 2048, 2>(m, rp, cols, vals, x, y, bounds, nb, lanes, s); break;
+    }
+  };
+  if (lanes > 0) go(std::true_type{});
+  else go(std::false_type{});
 }
 
 template <class T>
 static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int workers,
                         const T* vals, const T* svals, const T* x, T* y, cudaStream_t s) {
   const int64_t n = m->nrows;
+  // the row kernel's bulk copies need 16-B aligned bases (every buffer of a
+  // handle comes from svb::alloc, which guarantees it)
+  for (const void* p : {(const void*)vals, (const void*)svals, (const void*)ptr<int>(m->cols),
+                        (const void*)ptr<int>(m->scols)})
+    SVB_REQUIRE(((uintptr_t)p & 15) == 0, SVB_INVALID, "matrix buffers must be 16-byte aligned");
   if (fmt == SVB_CSR) {
     if (lib == SVB_LIBA && !(lane == 2 || lane == 4 || lane == 8 || lane == 16 || lane == 32))
       throw Error{SVB_UNSUPPORTED_CONFIG, "lane_width must be one of (2, 4, 8, 16, 32)"};
@@ -573,25 +967,18 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
       }
       bounds = device_bounds(m, workers, &nb, s);
     }
-    const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
     if (m->ptr64)
-      k_csr_rowseg<T, long long, false><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                                                  vals, x, y, bounds, nb, lanes);
+      launch_rows<T, long long, false>(m, ptr<long long>(m->ptr), ptr<int>(m->cols), vals, x, y, bounds, nb, lanes, s);
     else
-      k_csr_rowseg<T, int, false><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<int>(m->ptr), ptr<int>(m->cols), vals, x, y,
-                                                            bounds, nb, lanes);
-    SVB_CUDA_TRY(cudaGetLastError());   // counted by the final check below
-    launch_long<T, false>(m, ptr<int>(m->cols), vals, x, y, bounds, nb, lanes, s);
+      launch_rows<T, int, false>(m, ptr<int>(m->ptr), ptr<int>(m->cols), vals, x, y, bounds, nb, lanes, s);
+    return;
   } else if (fmt == SVB_COO) {
     if (lib == SVB_LIBA) {
       // row runs of the sorted coordinates (kernels.py:141-153), reduced in
       // reduceat order by the row kernel; rows without entries get 0
       const long long* runs = coo_runs(m, s);
-      const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
-      k_csr_rowseg<T, long long, false><<<g, ROWSEG_ROWS, 0, s>>>(n, runs, ptr<int>(m->cols), vals, x, y,
-                                                                  nullptr, 0, 0);
-      SVB_CUDA_TRY(cudaGetLastError());
-      launch_long<T, false>(m, ptr<int>(m->cols), vals, x, y, nullptr, 0, 0, s);
+      launch_rows<T, long long, false>(m, runs, ptr<int>(m->cols), vals, x, y, nullptr, 0, 0, s);
+      return;
     } else {
       SVB_CUDA_TRY(cudaMemsetAsync(y, 0, n * sizeof(T), s));
       if (m->nnz == 0) return;
@@ -610,14 +997,10 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
     k_dia<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), vals, x, y);
   } else {  // HYB
     k_ell_sweep<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), vals, x, y);
-    if (m->spill_nnz > 0) {
-      SVB_CHECK_LAUNCH();
-      const unsigned g = (unsigned)((n + ROWSEG_ROWS - 1) / ROWSEG_ROWS);
-      k_csr_rowseg<T, long long, true><<<g, ROWSEG_ROWS, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int>(m->scols),
-                                                                 svals, x, y, nullptr, 0, 0);
-      SVB_CUDA_TRY(cudaGetLastError());
-      launch_long<T, true>(m, ptr<int>(m->scols), svals, x, y, nullptr, 0, 0, s);
-    }
+    SVB_CHECK_LAUNCH();
+    if (m->spill_nnz > 0)
+      launch_rows<T, long long, true>(m, ptr<long long>(m->ptr), ptr<int>(m->scols), svals, x, y, nullptr, 0, 0, s);
+    return;
   }
   SVB_CHECK_LAUNCH();
 }

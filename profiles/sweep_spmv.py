@@ -6,6 +6,7 @@ against the measured HBM copy peak.
     python profiles/sweep_spmv.py [runs] > profiles/r1_spmv_sweep.json
 """
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -64,7 +65,10 @@ def main():
         y = device.DeviceVector(n)
         res = {}
         reps = {}
+        only = os.environ.get("SWEEP_TOKENS")
         for cfg in P.enumerate_configs():
+            if only and cfg.token() not in only.split(","):
+                continue
             f = cfg.format
             if f not in reps:
                 try:
