@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "matrix.cuh"
+#include "mgs_tma.cuh"
 
 struct svb_krylov {
   int64_t n = 0, ld = 0;
@@ -34,6 +35,12 @@ struct svb_krylov {
   size_t tmem_smem = 0;
   int normalized = -1;
   svb::Buf gparts;
+  // TMA-streamed MGS (mgs_tma.cuh, the default when the slice fits): launch
+  // plan, tagged exchange slots and the per-launch epoch of the tags
+  bool tma = false;
+  int tma_chunks = 0, tma_stages = 0;
+  unsigned long long epoch = 0;
+  svb::Buf gslot;
   // recorded right after every status-producing kernel: the host waits on
   // this, not on the stream, so work enqueued behind it (the speculative
   // next SpMV, CG's p update) overlaps the host's decision
@@ -977,6 +984,23 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
         // full 512-column TMEM allocation can never contend
         const bool tmem_ok = !(mode && std::strcmp(mode, "resident") == 0) &&
                              (k->chunk + PB - 1) / PB <= TMEM_MAX_PER_THREAD;
+        // TMA-streamed MGS: w in registers + smem, V_{i-1} in TMEM, the basis
+        // rows streamed once through a bulk-copy ring
+        const bool tma_ok = !(mode && (std::strcmp(mode, "resident") == 0 || std::strcmp(mode, "tmem") == 0)) &&
+                            m + 2 < 255;
+        if (k->resident && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages) &&
+            mgs::SMEM <= (size_t)optin) {
+          SVB_CUDA_TRY(cudaFuncSetAttribute(mgs::k_mgs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)mgs::SMEM));
+          int per = 0;
+          SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mgs::k_mgs_tma, mgs::NT, mgs::SMEM));
+          if (per >= 1) {
+            k->tma = true;
+            const size_t gb = 2 * (size_t)mgs::SLOT_STRIDE * G * sizeof(unsigned long long);
+            k->gslot = alloc(gb, s);
+            SVB_CUDA_TRY(cudaMemsetAsync(k->gslot->ptr, 0, gb, s));
+          }
+        }
         if (k->resident && tmem_ok) {
           k->tmem_smem = std::max<size_t>(k->res_smem, 120 * 1024);
           if (k->tmem_smem <= (size_t)optin) {
@@ -1073,6 +1097,33 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
     SVB_REQUIRE(j >= 0 && j < k->m, SVB_INVALID, "Arnoldi column out of range");
     Gm G = gm_of(k);
     cudaStream_t s = S(stream);
+    if (k->tma) {
+      mgs::Args A{};
+      A.V = G.V;
+      A.n = G.n;
+      A.ld = G.ld;
+      A.chunk = k->chunk;
+      A.m = G.m;
+      A.j = j;
+      A.H = G.H;
+      A.cs = G.cs;
+      A.sn = G.sn;
+      A.g = G.g;
+      A.st = G.st;
+      A.bnorm = bnorm;
+      A.gslot = ptr<unsigned long long>(k->gslot);
+      A.epoch = ++k->epoch;
+      A.chunk_count = k->tma_chunks;
+      A.nsb = k->tma_stages;
+      A.trace = nullptr;
+      void* args[] = {&A};
+      SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)mgs::k_mgs_tma, dim3(sm_count()), dim3(mgs::NT), args,
+                                               mgs::SMEM, s));
+      note_launches(1);
+      k->normalized = j;
+      mark(k, s);
+      return;
+    }
     if (k->resident) {
       int64_t chunk = k->chunk;
       double* gp = ptr<double>(k->gparts);
