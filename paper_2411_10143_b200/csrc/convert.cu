@@ -275,11 +275,21 @@ __global__ void k_spill_fill(int64_t nrows, int64_t width, const int64_t* __rest
 
 // diagonal occupancy bitmap: bit (col - row + nrows - 1); test before the
 // atomic so the hot diagonals of banded matrices are not contended
-__global__ void k_diag_bits(int64_t nrows, const int64_t* __restrict__ ptr, const int* __restrict__ cols,
-                            unsigned* __restrict__ bits) {
-  GRID_STRIDE(i, nrows) {
-    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
-      const int64_t d = (int64_t)cols[k] - i + nrows - 1;
+// diagonal-occupancy bitmap over row tiles staged in shared memory (coalesced
+// col_idx reads); a bit is only atomically set when it is still clear
+constexpr int TILE_ROWS = 256;
+__global__ void __launch_bounds__(TILE_ROWS) k_diag_bits(int64_t nrows, const int64_t* __restrict__ ptr,
+                                                         const int* __restrict__ cols, unsigned* __restrict__ bits) {
+  constexpr int CAP = 8192;
+  __shared__ int scol[CAP];
+  const int64_t ntiles = (nrows + TILE_ROWS - 1) / TILE_ROWS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const StagedRows<int64_t> t = stage_row_tile<int64_t, TILE_ROWS, CAP>(tile, nrows, ptr, cols, scol);
+    const int64_t i = t.r0 + threadIdx.x;
+    if (i >= t.r1) continue;
+    for (int64_t k = ptr[i] - t.base, e = ptr[i + 1] - t.base; k < e; ++k) {
+      const int c = t.staged ? scol[k] : __ldg(cols + t.base + k);
+      const int64_t d = (int64_t)c - i + nrows - 1;
       const unsigned m = 1u << (d & 31);
       unsigned* w = bits + (d >> 5);
       if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
@@ -306,21 +316,37 @@ __global__ void k_bits_to_offsets(int64_t nwords, int64_t nrows, const unsigned*
 
 constexpr int DIA_CAP = 4096;  // DIA_OFFSET_CAP (formats.py:18)
 
-__global__ void k_dia_scatter(int64_t nrows, int64_t ndiag, const long long* __restrict__ offs,
-                              const int64_t* __restrict__ ptr, const int* __restrict__ cols,
-                              const double* __restrict__ vals, double* __restrict__ data) {
-  __shared__ long long so[DIA_CAP];
+// DIA data, every cell written once (no memset): thread-per-row over a row
+// tile staged in shared memory; the row's (strictly increasing) columns are
+// merged against the ascending offsets, so data[d*n + i] is the value at
+// column i + off[d] or 0.  Consecutive threads write consecutive rows of
+// each diagonal: coalesced stores.  Dynamic smem: offsets, tile cols, vals.
+constexpr int DIA_TILE_CAP = 4096;
+__global__ void __launch_bounds__(TILE_ROWS) k_csr_to_dia(int64_t nrows, int64_t ndiag, const long long* __restrict__ offs,
+                                                        const int64_t* __restrict__ ptr, const int* __restrict__ cols,
+                                                        const double* __restrict__ vals, double* __restrict__ data) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* sval = reinterpret_cast<double*>(dsm);
+  long long* so = reinterpret_cast<long long*>(sval + DIA_TILE_CAP);
+  int* scol = reinterpret_cast<int*>(so + ndiag);
   for (int k = threadIdx.x; k < ndiag; k += blockDim.x) so[k] = offs[k];
-  __syncthreads();
-  GRID_STRIDE(i, nrows) {
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
-      const long long d = (long long)cols[e] - i;
-      int lo = 0, hi = (int)ndiag;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (so[mid] < d) lo = mid + 1; else hi = mid;
+  const int64_t ntiles = (nrows + TILE_ROWS - 1) / TILE_ROWS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const StagedRows<int64_t> t =
+        stage_row_tile<int64_t, TILE_ROWS, DIA_TILE_CAP>(tile, nrows, ptr, cols, scol, vals, sval);
+    const int64_t i = t.r0 + threadIdx.x;
+    if (i >= t.r1) continue;
+    int64_t k = ptr[i] - t.base;
+    const int64_t e = ptr[i + 1] - t.base;
+    int c = k < e ? (t.staged ? scol[k] : __ldg(cols + t.base + k)) : 0;
+    for (int64_t d = 0; d < ndiag; ++d) {
+      double v = 0.0;
+      if (k < e && (long long)c - i == so[d]) {
+        v = t.staged ? sval[k] : __ldg(vals + t.base + k);
+        ++k;
+        if (k < e) c = t.staged ? scol[k] : __ldg(cols + t.base + k);
       }
-      data[(int64_t)lo * nrows + i] = vals[e];
+      data[d * nrows + i] = v;
     }
   }
 }
@@ -390,7 +416,7 @@ static svb_matrix* build_dia(const RowView& v, cudaStream_t s) {
   Buf bits = alloc(nwords * 4, s);
   SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
   if (v.nnz) {
-    k_diag_bits<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+    k_diag_bits<<<grid_for(v.nrows, TILE_ROWS), TILE_ROWS, 0, s>>>(v.nrows, ptr<int64_t>(v.ptr), ptr<int>(v.cols),
                                                        ptr<unsigned>(bits));
     SVB_CHECK_LAUNCH();
   }
@@ -411,10 +437,16 @@ static svb_matrix* build_dia(const RowView& v, cudaStream_t s) {
     k_bits_to_offsets<<<grid_for(nwords, 256), 256, 0, s>>>(nwords, v.nrows, ptr<unsigned>(bits),
                                                             ptr<int64_t>(pos), ptr<long long>(m->offs));
     SVB_CHECK_LAUNCH();
-    SVB_CUDA_TRY(cudaMemsetAsync(m->vals->ptr, 0, ndiag * v.nrows * 8, s));
-    k_dia_scatter<<<grid_for(v.nrows, 256), 256, 0, s>>>(v.nrows, ndiag, ptr<long long>(m->offs),
-                                                         ptr<int64_t>(v.ptr), ptr<int>(v.cols),
-                                                         ptr<double>(v.vals), ptr<double>(m->vals));
+    const size_t dsm = (size_t)DIA_TILE_CAP * 12 + (size_t)ndiag * 8;
+    static bool attr = false;
+    if (!attr) {
+      SVB_CUDA_TRY(cudaFuncSetAttribute(k_csr_to_dia, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)((size_t)DIA_TILE_CAP * 12 + (size_t)DIA_CAP * 8)));
+      attr = true;
+    }
+    k_csr_to_dia<<<grid_for(v.nrows, TILE_ROWS, 4), TILE_ROWS, dsm, s>>>(v.nrows, ndiag, ptr<long long>(m->offs),
+                                                                   ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+                                                                   ptr<double>(v.vals), ptr<double>(m->vals));
     SVB_CHECK_LAUNCH();
     m->h_offs.resize(ndiag);
     SVB_CUDA_TRY(cudaMemcpyAsync(m->h_offs.data(), m->offs->ptr, ndiag * 8, cudaMemcpyDeviceToHost, s));

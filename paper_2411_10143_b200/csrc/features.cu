@@ -55,25 +55,32 @@ template <class P, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __restrict__ ptr,
                                                     const int* __restrict__ cols,
                                                     unsigned* __restrict__ bits, FeatAcc* out) {
+  constexpr int CAP = 8192;  // staged column indices per tile (32 KB)
+  __shared__ int scol[CAP];
   FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = ptr[i], e = ptr[i + 1], L = e - s;
+  const int64_t ntiles = (nrows + BLOCK - 1) / BLOCK;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const StagedRows<P> t = stage_row_tile<P, BLOCK, CAP>(tile, nrows, ptr, cols, scol);
+    const int64_t i = t.r0 + threadIdx.x;
+    if (i >= t.r1) continue;
+    const int64_t s = (int64_t)ptr[i] - t.base, e = (int64_t)ptr[i + 1] - t.base, L = e - s;
+    auto col = [&](int64_t k) { return t.staged ? scol[k] : __ldg(cols + t.base + k); };
     a.sum_r += (unsigned long long)L;
     a.sum_r2 += (unsigned long long)(L * L);
     a.max_r = max(a.max_r, (long long)L);
     a.min_r = min(a.min_r, (long long)L);
     if (L == 0) continue;
     const int64_t diag0 = nrows - 1 - i;
-    int c0 = cols[s], prev = c0;
+    const int c0 = col(s);
+    int prev = c0;
     int64_t run = 1, best = 1;
-    for (int64_t k = s;; ) {
+    for (int64_t k = s;;) {
       const int64_t d = (int64_t)prev + diag0;
       const unsigned m = 1u << (d & 31);
       unsigned* w = bits + (d >> 5);
       if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
       if (++k >= e) break;
-      const int c = cols[k];
+      const int c = col(k);
       run = (c == prev + 1) ? run + 1 : 1;
       best = max(best, run);
       prev = c;

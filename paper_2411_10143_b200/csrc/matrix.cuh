@@ -81,4 +81,40 @@ void forget_bounds(const svb_matrix* m);  // drop cached LibC chunk bounds (spmv
 // copied back to the host (synchronises `s`)
 int64_t exclusive_scan_total(const int64_t* counts, int64_t* out, int64_t n, cudaStream_t s);
 
+// ---------------------------------------------------------------------------
+// Row tiles staged through shared memory.  Thread-per-row kernels over CSR
+// read col_idx with a stride of one row per lane (poorly coalesced); a CTA
+// instead copies the contiguous nnz range of its BLOCK rows into shared
+// memory with coalesced loads and lets each thread walk its row there.
+// Tiles whose nnz exceed the capacity are walked straight from global
+// memory (staged == false).  Call from every thread of the CTA.
+// ---------------------------------------------------------------------------
+template <class P>
+struct StagedRows {
+  int64_t r0, r1, base;
+  bool staged;
+};
+
+template <class P, int BLOCK, int CAP>
+__device__ __forceinline__ StagedRows<P> stage_row_tile(int64_t tile, int64_t nrows, const P* __restrict__ ptr,
+                                                     const int* __restrict__ cols, int* scols,
+                                                     const double* __restrict__ vals = nullptr,
+                                                     double* svals = nullptr) {
+  StagedRows<P> t;
+  t.r0 = tile * BLOCK;
+  t.r1 = t.r0 + BLOCK < nrows ? t.r0 + BLOCK : nrows;
+  t.base = (int64_t)ptr[t.r0];
+  const int64_t cnt = (int64_t)ptr[t.r1] - t.base;
+  t.staged = cnt <= CAP;
+  __syncthreads();  // the previous tile's readers are done with the buffers
+  if (t.staged) {
+    for (int64_t k = threadIdx.x; k < cnt; k += BLOCK) {
+      scols[k] = __ldg(cols + t.base + k);
+      if (svals) svals[k] = __ldg(vals + t.base + k);
+    }
+  }
+  __syncthreads();
+  return t;
+}
+
 }  // namespace svb

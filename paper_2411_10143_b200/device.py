@@ -2,8 +2,10 @@
 
 Nothing here computes; it only moves bytes and orders work.  Solver and
 advisor work run on separate non-blocking CUDA streams (the advisor's at the
-lowest priority) so the paper's predict-while-solve overlap happens on the
-device, not just in host threads.
+highest priority: its few short kernels are dispatched ahead of the solver's
+queue instead of starving behind the persistent Arnoldi kernels) so the
+paper's predict-while-solve overlap happens on the device, not just in host
+threads.
 """
 from __future__ import annotations
 

@@ -11,6 +11,9 @@ sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
+if "torch" in sys.argv:
+    import torch  # noqa: E402,F401
+    torch.cuda.set_device(0)
 import paper_2411_10143_b200 as P  # noqa: E402
 from paper_2411_10143_b200 import _lib, device, solver  # noqa: E402
 from paper_2411_10143_b200.solver import DeviceOptions  # noqa: E402
@@ -74,9 +77,12 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 8):
         first.setdefault(it, t)
     its = sorted(first)
     gaps = [round((first[its[k]] - first[its[k - 1]]) * 1e3, 2) for k in range(1, min(len(its), 12))]
+    allg = [(first[its[k]] - first[its[k - 1]], its[k]) for k in range(1, len(its))]
+    worst = max(allg) if allg else (0.0, 0)
     out.append({"wall_ms": round(wall * 1e3, 1), "swaps": [(x.iteration, x.config.token(),
                 round(x.swap_cost_seconds * 1e3, 2)) for x in r.config_timeline],
                 "first_iter_gaps_ms": gaps, "iters": r.iterations,
+                "worst_gap": (round(worst[0] * 1e3, 2), worst[1]),
                 "free_gb": round(device.device_info()["free_bytes"] / 1e9, 2),
                 "pool_gb": [round(device.device_info()[k] / 1e9, 2)
                             for k in ("pool_reserved_bytes", "pool_used_bytes")]})
