@@ -18,8 +18,12 @@ solution therefore includes all preprocessing.
            reference) on the host cores, bounded sample (oracle/bench_cpu.py)
 
 `--impl reference` prints the reference arm (CPU oracle port) instead.
-Multi-GPU (torchrun): every rank solves its own replica (weak scaling; the
-row-partitioned solver is not in this round), value = max over ranks.
+Multi-GPU (torchrun, N > 1): the row-partitioned solver (distributed.py) on
+the same config-2 problem — each rank generates its slab on its GPU, the
+cascade runs on exact global features, SpMV halos and dot products go over
+NCCL (strong scaling, value = max over ranks).  `--workload config5` runs
+BASELINE configs[4] (row-partitioned CG, 27-point Laplacian 600^3) the same
+way at any N, including N = 1.
 """
 from __future__ import annotations
 
@@ -313,9 +317,14 @@ def b200_arm(args):
     from paper_2411_10143_b200.solver import DeviceOptions
 
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or args.workload == "config5":
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=rank, world_size=ws,
+                                    device_id=torch.device("cuda", local))
+        return dist_arm(args, ws, rank, local)
     L = _lib.lib()
 
     def barrier():
@@ -529,6 +538,139 @@ def b200_arm(args):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# row-partitioned arm (torchrun, N > 1; or --workload config5 at any N)
+# ---------------------------------------------------------------------------
+def stencil_problem(workload: str):
+    if workload == "config5":
+        offs, wts = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    offs.append((dz, dy, dx))
+                    wts.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+        n3 = int(os.environ.get("SPMVTUNE_CONFIG5_N", "600"))
+        return ("cg", (n3, n3, n3), offs, wts,
+                f"config5: CG fp64, tol {TOL:g}, b=A*1, 3-D 27-point Laplacian {n3}^3 "
+                f"(n={n3 ** 3:,}, nnz={(3 * n3 - 2) ** 3:,}), row-partitioned z-slabs generated "
+                "per rank on the device, cascade on exact global features, NCCL halo + all-reduce")
+    offs, wts = [], []
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            offs.append((dy, dx))
+            wts.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
+    return ("gmres", (NX, NX), offs, wts, WORKLOAD.replace("async predict-while-solve starting on "
+            "CSR/LibA/32", "row-partitioned predict-then-solve (cascade on exact global features, "
+            "NCCL halo + all-reduce)"))
+
+
+def dist_arm(args, ws, rank, local):
+    """Time-to-solution of the row-partitioned solve (distributed.py): each
+    rank generates its slab on its GPU (outside the clock, like the single-GPU
+    arm's matrix), then every step runs global features -> cascade ->
+    conversion -> solve.  Strong scaling: the problem is fixed as N grows."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_10143_b200 as P
+    from paper_2411_10143_b200 import _lib, device
+    from paper_2411_10143_b200.distributed import distributed_stencil_solve, stencil_block, \
+        stencil_partition
+
+    method, dims, offs, wts, workload = stencil_problem(args.workload)
+    models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
+    params = P.GmresParams(restart_m=RESTART, tol=TOL, max_iters=20000)
+    bounds = stencil_partition(dims, ws)
+    s = device.thread_stream(0)
+    t0 = time.perf_counter()
+    blk = stencil_block(dims, offs, wts, int(bounds[rank]), int(bounds[rank + 1]), s)
+    gen_s = time.perf_counter() - t0
+
+    def step():
+        t = {}
+        res, _ = distributed_stencil_solve(method, dims, offs, wts, params, models=models, blk=blk,
+                                           timings=t)
+        return res, t
+
+    for _ in range(args.warmup):
+        step()
+    try:
+        clocks = NvmlClockSampler(local)
+    except Exception:
+        clocks = ClockSampler(local)
+    launches0 = _lib.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    steps, results = [], []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        res, t = step()
+        steps.append(t)
+        results.append({k: res[k] for k in ("converged", "iterations", "final", "config")})
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_all
+    dist.barrier()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    tt = torch.tensor([wall], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    value = float(tt.item()) / args.steps
+
+    # roofline: the local SpMV in the predicted configuration, events on our stream
+    cfg = P.SpmvConfig.from_token(results[-1]["config"])
+    csr = blk._dev_csr
+    mat = csr if cfg.format is P.FormatTag.CSR else P.convert(csr, cfg.format)
+    inf = mat._device().info
+    xw = device.DeviceVector(blk.window)
+    _lib.check(_lib.lib().svb_fill(xw.ptr, blk.window, 1.0, s.handle))
+    yl = device.DeviceVector(blk.nloc)
+    ext = torch.cuda.ExternalStream(s.handle)
+    from paper_2411_10143_b200.kernels import default_workers, launch
+    for _ in range(3):
+        launch(cfg, mat, xw.ptr, yl.ptr, workers=default_workers(), stream=s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record(ext)
+    for _ in range(reps):
+        launch(cfg, mat, xw.ptr, yl.ptr, workers=default_workers(), stream=s)
+    e1.record(ext)
+    torch.cuda.synchronize()
+    spmv_ms = e0.elapsed_time(e1) / reps
+    n_loc = blk.nloc
+    info = {"nnz": int(inf.nnz), "ndiag": int(inf.ndiag), "width": int(inf.width),
+            "spill": int(inf.spill_nnz)}
+    byts = algorithmic_bytes("spmv:" + cfg.token(), info, n_loc)
+    byts += 8 * (blk.window - n_loc)          # x is the window, not just the local rows
+    hbm, peak_kind = peaks()
+    gbs = byts / (spmv_ms / 1e3) / 1e9
+    roofline = {"kernel": "spmv:" + cfg.token(), "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(gbs / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_launch": byts, "avg_launch_ms": spmv_ms}
+    its = results[-1]["iterations"]
+    per_iter = {k: v / max(1, its) for k, v in steps[-1].items() if k == "solve_s"}
+    gathered = [None] * ws
+    dist.all_gather_object(gathered, {"rank": rank, "rows": [int(bounds[rank]), int(bounds[rank + 1])],
+                                      "spmv_ms": spmv_ms, "gbs": gbs, "gen_s": gen_s,
+                                      "last_step": steps[-1]})
+    if rank == 0:
+        line = {"metric": "CG/GMRES time-to-solution incl. preprocessing (global features+cascade+"
+                          "conversion), row-partitioned",
+                "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "parallelism": f"row-partitioned x{ws}",
+                           "l2": "inputs larger than L2"},
+                "roofline": roofline, "cpu_baseline": None,
+                "e2e": None, "gpu_launches": int(launches), "clocks": clk,
+                "detail": {"results": results[-1], "per_step": steps, "per_rank": gathered,
+                           "per_iteration_solve_s": per_iter,
+                           "cpu_baseline_note": "the reference arm's CPU path cannot hold this "
+                           "matrix (int64 CSR >= 140 GB) — see BASELINE configs[4]"
+                           if args.workload == "config5" else "single-GPU line carries it"}}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -539,6 +681,9 @@ def main(argv=None):
                     help="reference arm: GMRES iterations the solve takes (77 at config 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-1 CG side measurement")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config5"],
+                    help="config5 = row-partitioned CG on the 27-point Laplacian 600^3 (any N); "
+                         "N > 1 always runs the row-partitioned solver")
     args = ap.parse_args(argv)
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("--steps >= 1 and --warmup >= 0")

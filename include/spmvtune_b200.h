@@ -140,6 +140,13 @@ int svb_matrix_download(const svb_matrix* m, int which, void* dst_host, void* st
  * axis last; offsets[nst*ndim]; weights[nst]. */
 int svb_csr_stencil(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
                     const double* weights, void* stream, svb_matrix** out);
+/* Rows [r0, r1) of the same stencil matrix as a row-partitioned rank's local
+ * block: ncols = cmax - cmin + 1 and column c is stored as
+ * c - cmin (the rank's column window, which must cover rows [r0, r1)).
+ * Generated on the device, so a 600^3 slab never exists on the host. */
+int svb_csr_stencil_rows(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
+                         const double* weights, int64_t r0, int64_t r1, int64_t cmin, int64_t cmax,
+                         void* stream, svb_matrix** out);
 
 /* ---- conversion: convert(m, target) (formats.py:302-320) ----------------
  * Bit-exact with the reference arrays.  DIA above 4096 diagonals returns
@@ -244,6 +251,8 @@ int svb_vec_axpby(svb_vecops* v, double a, const double* x_dev, double b, double
                   void* stream);
 /* x *= s */
 int svb_vec_scale(svb_vecops* v, double* x_dev, double s, void* stream);
+/* x[0..n) = v on the device (row-partitioned setup: windows of ones) */
+int svb_fill(double* x_dev, int64_t n, double v, void* stream);
 
 /* ---- compiled cascade inference (inference.py:55-125, model_schema.md) ---
  * Flattened tree ensemble: node arrays in the reference's flattening order;

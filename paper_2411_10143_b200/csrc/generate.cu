@@ -38,25 +38,27 @@ __device__ __forceinline__ bool inside(const Stencil& st, const int64_t* c, int 
   return true;
 }
 
-__global__ void k_stencil_count(Stencil st, int64_t n, int64_t* __restrict__ cnt) {
+// rows [r0, r0 + n) of the global stencil matrix
+__global__ void k_stencil_count(Stencil st, int64_t n, int64_t r0, int64_t* __restrict__ cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[MAX_DIM];
-    coords_of(st, i, c);
+    coords_of(st, r0 + i, c);
     int64_t k = 0;
     for (int s = 0; s < st.nst; ++s) k += inside(st, c, s);
     cnt[i] = k;
   }
 }
 
-__global__ void k_stencil_fill(Stencil st, int64_t n, const int64_t* __restrict__ ptr, int* __restrict__ cols,
-                               double* __restrict__ vals) {
+// columns stored relative to `cmin` (a row block's column window)
+__global__ void k_stencil_fill(Stencil st, int64_t n, int64_t r0, int64_t cmin, const int64_t* __restrict__ ptr,
+                               int* __restrict__ cols, double* __restrict__ vals) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[MAX_DIM];
-    coords_of(st, i, c);
+    coords_of(st, r0 + i, c);
     int64_t o = ptr[i];
     for (int s = 0; s < st.nst; ++s) {
       if (!inside(st, c, s)) continue;
-      cols[o] = (int)(i + st.lin[s]);
+      cols[o] = (int)(r0 + i + st.lin[s] - cmin);
       vals[o] = st.w[s];
       ++o;
     }
@@ -67,63 +69,84 @@ __global__ void k_stencil_fill(Stencil st, int64_t n, const int64_t* __restrict_
 
 using namespace svb;
 
+static svb_matrix* stencil_rows(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
+                                const double* weights, int64_t r0, int64_t r1, int64_t cmin, int64_t ncols,
+                                cudaStream_t s) {
+  SVB_REQUIRE(ndim >= 1 && ndim <= MAX_DIM && nst >= 1 && nst <= MAX_ST, SVB_INVALID,
+              "stencil: 1..4 dimensions, 1..128 points");
+  Stencil st{};
+  st.ndim = ndim;
+  st.nst = nst;
+  int64_t N = 1;
+  for (int a = 0; a < ndim; ++a) {
+    SVB_REQUIRE(dims[a] >= 1, SVB_INVALID, "stencil: grid dimensions must be positive");
+    st.dims[a] = dims[a];
+    N *= dims[a];
+  }
+  SVB_REQUIRE(0 <= r0 && r0 < r1 && r1 <= N, SVB_INVALID, "stencil: bad row range");
+  SVB_REQUIRE(ncols < INT32_MAX, SVB_INAPPLICABLE, "stencil column window exceeds the int32 index range");
+  std::vector<int64_t> lin(nst);
+  for (int k = 0; k < nst; ++k) {
+    int64_t l = 0, stride = 1;
+    for (int a = ndim - 1; a >= 0; --a) {
+      l += (int64_t)offsets[k * ndim + a] * stride;
+      stride *= dims[a];
+    }
+    lin[k] = l;
+  }
+  std::vector<int> order(nst);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lin[a] < lin[b]; });
+  for (int k = 0; k < nst; ++k) {
+    const int src = order[k];
+    for (int a = 0; a < ndim; ++a) st.off[k][a] = offsets[src * ndim + a];
+    st.lin[k] = lin[src];
+    st.w[k] = weights[src];
+  }
+  const int64_t n = r1 - r0;
+  Buf cnt = alloc(n * 8, s);
+  k_stencil_count<<<grid_for(n, 256), 256, 0, s>>>(st, n, r0, ptr<int64_t>(cnt));
+  SVB_CHECK_LAUNCH();
+  Buf ptr64 = alloc((n + 1) * 8, s);
+  const int64_t nnz = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(ptr64), n, s);
+  cnt.reset();
+  auto m = new svb_matrix();
+  m->fmt = SVB_CSR;
+  m->nrows = n;
+  m->ncols = ncols;
+  m->nnz = nnz;
+  m->ptr64 = nnz >= INT32_MAX;
+  m->cols = alloc(nnz * 4, s);
+  m->vals = alloc(nnz * 8, s);
+  k_stencil_fill<<<grid_for(n, 256), 256, 0, s>>>(st, n, r0, cmin, ptr<int64_t>(ptr64), ptr<int>(m->cols),
+                                                 ptr<double>(m->vals));
+  SVB_CHECK_LAUNCH();
+  if (m->ptr64) m->ptr = ptr64;
+  else {
+    m->ptr = alloc((n + 1) * 4, s);
+    narrow_i64_to_i32(ptr<int64_t>(ptr64), ptr<int32_t>(m->ptr), n + 1, s);
+  }
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  return publish(m);
+}
+
 extern "C" int svb_csr_stencil(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
                                const double* weights, void* stream, svb_matrix** out) {
   return guard([&] {
-    SVB_REQUIRE(ndim >= 1 && ndim <= MAX_DIM && nst >= 1 && nst <= MAX_ST, SVB_INVALID,
-                "stencil: 1..4 dimensions, 1..128 points");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    Stencil st{};
-    st.ndim = ndim;
-    st.nst = nst;
     int64_t n = 1;
-    for (int a = 0; a < ndim; ++a) {
-      SVB_REQUIRE(dims[a] >= 1, SVB_INVALID, "stencil: grid dimensions must be positive");
-      st.dims[a] = dims[a];
-      n *= dims[a];
-    }
+    for (int a = 0; a < ndim && a < MAX_DIM; ++a) n *= dims[a] > 0 ? dims[a] : 1;
     SVB_REQUIRE(n < INT32_MAX, SVB_INAPPLICABLE, "stencil grid exceeds the int32 column index range");
-    // sort the stencil points by linear offset so columns come out ascending
-    std::vector<int64_t> lin(nst);
-    for (int k = 0; k < nst; ++k) {
-      int64_t l = 0, stride = 1;
-      for (int a = ndim - 1; a >= 0; --a) {
-        l += (int64_t)offsets[k * ndim + a] * stride;
-        stride *= dims[a];
-      }
-      lin[k] = l;
-    }
-    std::vector<int> order(nst);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lin[a] < lin[b]; });
-    for (int k = 0; k < nst; ++k) {
-      const int src = order[k];
-      for (int a = 0; a < ndim; ++a) st.off[k][a] = offsets[src * ndim + a];
-      st.lin[k] = lin[src];
-      st.w[k] = weights[src];
-    }
-    Buf cnt = alloc(n * 8, s);
-    k_stencil_count<<<grid_for(n, 256), 256, 0, s>>>(st, n, ptr<int64_t>(cnt));
-    SVB_CHECK_LAUNCH();
-    Buf ptr64 = alloc((n + 1) * 8, s);
-    const int64_t nnz = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(ptr64), n, s);
-    cnt.reset();
-    auto m = new svb_matrix();
-    m->fmt = SVB_CSR;
-    m->nrows = m->ncols = n;
-    m->nnz = nnz;
-    m->ptr64 = nnz >= INT32_MAX;
-    m->cols = alloc(nnz * 4, s);
-    m->vals = alloc(nnz * 8, s);
-    k_stencil_fill<<<grid_for(n, 256), 256, 0, s>>>(st, n, ptr<int64_t>(ptr64), ptr<int>(m->cols),
-                                                   ptr<double>(m->vals));
-    SVB_CHECK_LAUNCH();
-    if (m->ptr64) m->ptr = ptr64;
-    else {
-      m->ptr = alloc((n + 1) * 4, s);
-      narrow_i64_to_i32(ptr<int64_t>(ptr64), ptr<int32_t>(m->ptr), n + 1, s);
-    }
-    SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    *out = publish(m);
+    *out = stencil_rows(ndim, dims, nst, offsets, weights, 0, n, 0, n, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" int svb_csr_stencil_rows(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
+                                    const double* weights, int64_t r0, int64_t r1, int64_t cmin, int64_t cmax,
+                                    void* stream, svb_matrix** out) {
+  return guard([&] {
+    SVB_REQUIRE(cmin <= r0 && cmax >= r1 - 1 && cmin >= 0, SVB_INVALID,
+                "stencil block: the column window must cover the block's own rows");
+    *out = stencil_rows(ndim, dims, nst, offsets, weights, r0, r1, cmin, cmax - cmin + 1,
+                        reinterpret_cast<cudaStream_t>(stream));
   });
 }

@@ -908,6 +908,11 @@ __global__ void __launch_bounds__(KB) k_dot(int64_t n, const double* __restrict_
   if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = tot;
 }
 
+__global__ void __launch_bounds__(KB) k_fill(double* __restrict__ x, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
 static Gm gm_of(svb_krylov* k) {
   Gm G;
   G.V = ptr<double>(k->V);
@@ -1305,6 +1310,14 @@ int svb_vec_axpby(svb_vecops* v, double a, const double* x, double b, double* y,
 int svb_vec_scale(svb_vecops* v, double* x, double s, void* stream) {
   return guard([&] {
     k_vscale<<<v->grid, KB, 0, S(stream)>>>(v->n, x, s);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_fill(double* x, int64_t n, double v, void* stream) {
+  return guard([&] {
+    if (n <= 0) return;
+    k_fill<<<grid_for(n, KB), KB, 0, S(stream)>>>(x, n, v);
     SVB_CHECK_LAUNCH();
   });
 }

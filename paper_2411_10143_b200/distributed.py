@@ -38,7 +38,8 @@ from .formats import CsrMatrix, FormatTag, convert
 from .kernels import Library, SpmvConfig, default_workers, launch
 
 __all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
-           "NcclComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve"]
+           "NcclComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
+           "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve"]
 
 
 # ---------------------------------------------------------------------------
@@ -93,6 +94,67 @@ def local_block(row_ptr, col_idx, values, r0: int, r1: int, ncols: int) -> Local
     offs = np.unique(cols - rows)
     return LocalBlock(r0, r1, cmin, cmax, lp, cols - cmin, np.asarray(values[s:e], np.float64),
                       int(ncols), offs)
+
+
+# ---------------------------------------------------------------------------
+# stencil matrices generated per rank on the device (configs 2 and 5 at
+# scale: a 600^3 slab never exists on the host)
+# ---------------------------------------------------------------------------
+def _stencil_lin(dims, offsets) -> np.ndarray:
+    dims = [int(d) for d in dims]
+    strides = np.cumprod([1] + dims[::-1][:-1])[::-1]
+    return np.asarray(offsets, dtype=np.int64).reshape(-1, len(dims)) @ strides
+
+
+def stencil_partition(dims, world: int) -> np.ndarray:
+    """Row bounds of `world` slabs of whole leading-axis planes (z-slabs for
+    a 3-D grid), as even as the plane count allows."""
+    planes = int(dims[0])
+    plane = int(np.prod([int(d) for d in dims[1:]], dtype=np.int64))
+    cuts = np.linspace(0, planes, world + 1).round().astype(np.int64)
+    return cuts * plane
+
+
+def stencil_block_window(dims, offsets, r0: int, r1: int):
+    """(cmin, cmax, global diagonal offsets present) of the slab rows
+    [r0, r1), which must be whole leading-axis planes."""
+    dims = [int(d) for d in dims]
+    offs = np.asarray(offsets, dtype=np.int64).reshape(-1, len(dims))
+    plane = int(np.prod(dims[1:], dtype=np.int64))
+    z0, z1 = r0 // plane, r1 // plane
+    lin = _stencil_lin(dims, offsets)
+    present = []
+    for o, l in zip(offs, lin):
+        ok = max(z0, -o[0]) < min(z1, dims[0] - o[0])
+        ok = ok and all(abs(int(o[a])) < dims[a] for a in range(1, len(dims)))
+        if ok:
+            present.append(int(l))
+    n = int(np.prod(dims, dtype=np.int64))
+    lo = min(present) if present else 0
+    hi = max(present) if present else 0
+    cmin = min(max(0, r0 + lo), r0)
+    cmax = max(min(n - 1, r1 - 1 + hi), r1 - 1)
+    return cmin, cmax, np.unique(np.asarray(present, dtype=np.int64))
+
+
+def stencil_block(dims, offsets, weights, r0: int, r1: int, stream=None) -> "LocalBlock":
+    """Rank-local block of a stencil matrix generated on this rank's GPU
+    (svb_csr_stencil_rows); no host copy of the rows is made."""
+    import ctypes
+    cmin, cmax, present = stencil_block_window(dims, offsets, r0, r1)
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    o = np.ascontiguousarray(offsets, dtype=np.int32).reshape(-1)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    from .formats import _new_handle
+    dev = _new_handle(_lib.lib().svb_csr_stencil_rows, int(d.size),
+                      d.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(w.size),
+                      o.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                      w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(r0), int(r1), int(cmin),
+                      int(cmax), stream.handle if stream is not None else None)
+    blk = LocalBlock(int(r0), int(r1), int(cmin), int(cmax), None, None, None,
+                     int(np.prod(d)), present)
+    blk._dev_csr = CsrMatrix._wrap(dev)
+    return blk
 
 
 @dataclass
@@ -273,15 +335,30 @@ class DistOperator:
         self.window = ops.vec(block.window)
         self.own = block.r0 - block.cmin
         self.mat = ops.prepare(block, cfg)
+        # no halo: the window is exactly this rank's rows (one rank, or a
+        # block-diagonal matrix), so the SpMV reads the source vector itself
+        self.no_halo = not self.plan.recvs and block.window == block.nloc
+        self._own = None
 
     def swap(self, cfg: SpmvConfig):
         self.cfg = cfg
         self.mat = self.ops.prepare(self.block, cfg)
 
+    def own_view(self):
+        """This rank's slice of the window buffer: a vector kept there (CG's
+        p) needs no copy before the halo exchange."""
+        if self._own is None:
+            self._own = self.ops.view(self.window, self.own, self.block.nloc)
+        return self._own
+
     def apply(self, src, dst):
         """dst = A_local * x, with x's local slice in ``src``."""
         b, ops = self.block, self.ops
-        ops.copy(ops.view(self.window, self.own, b.nloc), ops.view(src, 0, b.nloc))
+        if self.no_halo:
+            ops.spmv(self.mat, self.cfg, src, dst)
+            return
+        if src is not self._own:
+            ops.copy(ops.view(self.window, self.own, b.nloc), ops.view(src, 0, b.nloc))
         sends = [(p, ops.view(src, lo - b.r0, hi - lo)) for p, lo, hi in self.plan.sends]
         recvs = [(p, ops.view(self.window, lo - b.cmin, hi - lo)) for p, lo, hi in self.plan.recvs]
         self.comm.exchange(sends, recvs)
@@ -410,7 +487,8 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     cg): one halo exchange + local SpMV and two scalar all-reduces per
     iteration."""
     ops, comm = A.ops, A.comm
-    x, r, p, q, bvec = ops.vec(), ops.vec(), ops.vec(), ops.vec(), ops.vec()
+    x, r, q, bvec = ops.vec(), ops.vec(), ops.vec(), ops.vec()
+    p = ops.vec() if A.no_halo else A.own_view()   # p lives in the halo window
     ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
         ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
     sc = ops.scalars(4)
@@ -486,6 +564,55 @@ def global_features(block: LocalBlock, nrows: int, ncols: int, nnz: int, comm, l
     runs = sum(a[5] for a in sums)
     ndiag = len(set().union(*[set(a[6]) for a in sums]))
     return features_from_aggregates(nrows, ncols, nnz, (s_r, s_r2, mx, mn, span, runs, ndiag))
+
+
+def distributed_stencil_solve(method: str, dims, offsets, weights, params, models=None,
+                              initial_config: SpmvConfig | None = None, blk: "LocalBlock | None" = None,
+                              timings: dict | None = None):
+    """Row-partitioned solve of a device-generated stencil matrix under
+    torchrun (NCCL), b = A*1 (solver.py:188-193).  Each rank generates its
+    z-slab on its own GPU (or reuses ``blk``); with ``models`` the cascade
+    runs on the exact global features (predict-then-solve).  Returns the
+    report dict (x stays on the device) and the block."""
+    import time
+
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    bounds = stencil_partition(dims, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    stream = device.thread_stream(0)
+    if blk is None:
+        blk = stencil_block(dims, offsets, weights, r0, r1, stream)
+    n = blk.ncols_global
+    ops, comm = CudaOps(blk.nloc, stream), NcclComm(stream)
+    csr = ops.local_csr(blk)
+    # b = A * 1 on this rank's rows (a window of ones times the local rows),
+    # outside the clock as in the reference (solver.py:355-358)
+    ones = ops.vec(blk.window)
+    _lib.check(_lib.lib().svb_fill(ones.ptr, blk.window, 1.0, stream.handle))
+    bvec = ops.vec()
+    _lib.check(_lib.lib().svb_spmv_sequential(csr._device().handle, ones.ptr, bvec.ptr, stream.handle))
+    del ones
+    stream.sync()
+    t0 = time.perf_counter()
+    cfg = initial_config or SpmvConfig(FormatTag.CSR, Library.LIB_B)
+    nnz = int(sum(comm.allgather_obj(int(csr.nnz))))
+    if models is not None:
+        from .inference import cascade_predict
+        fv = global_features(blk, n, n, nnz, comm, csr, stream)
+        cfg = cascade_predict(models, fv)
+    t1 = time.perf_counter()
+    A = DistOperator(blk, bounds, comm, ops, cfg)
+    stream.sync()
+    t2 = time.perf_counter()
+    res = (dist_cg if method == "cg" else dist_gmres)(A, bvec, params)
+    stream.sync()
+    t3 = time.perf_counter()
+    res["config"] = cfg.token()
+    if timings is not None:
+        timings.update({"predict_s": t1 - t0, "convert_s": t2 - t1, "solve_s": t3 - t2,
+                        "total_s": t3 - t0})
+    return res, blk
 
 
 def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=None,

@@ -195,3 +195,45 @@ def test_stencil_halo_is_neighbour_planes():
         peers = sorted(p for p, _, _ in plan.recvs)
         assert peers == [p for p in (r - 1, r + 1) if 0 <= p < 4]
         assert plan.bytes_per_exchange() <= 8 * 2 * (12 * 12 + 12 + 1)
+
+
+def _stencil27():
+    offs, w = [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                offs.append((dz, dy, dx))
+                w.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+    return offs, w
+
+
+@pytest.mark.parametrize("dims,world", [((7, 5, 4), 3), ((9, 6), 4), ((4, 3, 3), 4), ((5, 5, 5), 1)])
+def test_stencil_slab_windows_cover_brute_force(dims, world):
+    """z-slab partition of a device-generated stencil: whole planes per rank,
+    and the column window / global diagonal set equal what the rows of the
+    host CSR hold (the device block generator relies on both)."""
+    from paper_2411_10143_b200.distributed import stencil_block_window, stencil_partition
+    if len(dims) == 3:
+        offs, w = _stencil27()
+    else:
+        offs = [(dy, dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+        w = [8.5 if o == (0, 0) else -1.0 for o in offs]
+    n, _, ptr, cols, _ = G.stencil_csr(dims, offs, w)
+    bounds = stencil_partition(dims, world)
+    plane = int(np.prod(dims[1:]))
+    assert bounds[0] == 0 and bounds[-1] == n and np.all(np.diff(bounds) >= 0)
+    assert np.all(bounds % plane == 0)
+    for r in range(world):
+        r0, r1 = int(bounds[r]), int(bounds[r + 1])
+        if r0 == r1:
+            continue
+        cmin, cmax, present = stencil_block_window(dims, offs, r0, r1)
+        c = cols[ptr[r0]:ptr[r1]]
+        rows = np.repeat(np.arange(r0, r1), np.diff(ptr[r0:r1 + 1]))
+        # the window covers every column the rows touch (it may be a few
+        # entries wider than the tight range: the generator bounds it by the
+        # stencil reach) and the diagonal set is exact
+        assert cmin <= min(int(c.min()), r0) and cmax >= max(int(c.max()), r1 - 1)
+        reach = int(np.abs(present).max())
+        assert cmin >= max(0, r0 - reach) and cmax <= min(n - 1, r1 - 1 + reach)
+        assert present.tolist() == np.unique(c - rows).tolist()
