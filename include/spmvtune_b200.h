@@ -100,6 +100,13 @@ int svb_event_record(void* stream, void** out);    /* new event, recorded on str
 int svb_event_query(void* event);                  /* SVB_OK when complete, else SVB_INVALID */
 int svb_stream_wait_event(void* stream, void* event);
 int svb_event_destroy(void* event);
+/* CUDA graph capture of work enqueued on `stream` by this thread (B200
+ * runtime: CG batches replay as one launch); replays count their kernels
+ * into svb_launch_count. */
+int svb_graph_begin(void* stream);
+int svb_graph_end(void* stream, void** graph_out);
+int svb_graph_launch(void* graph, void* stream);
+int svb_graph_destroy(void* graph);
 int svb_malloc(int64_t bytes, void** out);         /* device memory (pool) */
 int svb_free(void* ptr);
 int svb_host_alloc(int64_t bytes, void** out);     /* pinned host memory */
@@ -200,6 +207,9 @@ int svb_krylov_destroy(svb_krylov* k);
  * -3 = tmp (matvec target); -4 = CG p; -5 = CG q; -6 = CG r */
 int svb_krylov_vec(svb_krylov* k, int which, double** out);
 int svb_krylov_status_get(svb_krylov* k, void* stream, svb_krylov_status* out);
+/* re-record the status event on `stream` (after a graph replay: an event
+ * recorded during stream capture is not a usable event afterwards) */
+int svb_krylov_mark(svb_krylov* k, void* stream);
 /* ||b|| into status.beta */
 int svb_krylov_bnorm(svb_krylov* k, void* stream);
 /* GMRES cycle start: r = b - tmp; beta = ||r||; V0 = r/beta; g = beta e1 */

@@ -1056,6 +1056,10 @@ int svb_krylov_vec(svb_krylov* k, int which, double** out) {
 
 static void mark(svb_krylov* k, cudaStream_t s) { SVB_CUDA_TRY(cudaEventRecord(k->ev, s)); }
 
+int svb_krylov_mark(svb_krylov* k, void* stream) {
+  return guard([&] { mark(k, S(stream)); });
+}
+
 int svb_krylov_status_get(svb_krylov* k, void* stream, svb_krylov_status* out) {
   return guard([&] {
     (void)stream;

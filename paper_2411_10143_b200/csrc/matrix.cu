@@ -7,6 +7,8 @@
 #include <cstring>
 #include <thread>
 
+#include <vector>
+
 #include "matrix.cuh"
 
 namespace svb {
@@ -244,6 +246,56 @@ int svb_stream_create(int priority, void** out) {
 int svb_stream_destroy(void* stream) {
   return guard([&] { SVB_CUDA_TRY(cudaStreamDestroy(S(stream))); });
 }
+// CUDA graphs: a host loop that enqueues many short launches per step (CG's
+// batches) is captured once and replayed, so the host pays one launch per
+// batch instead of several per iteration.
+struct svb_graph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;   // kernel nodes, counted into svb_launch_count per replay
+};
+int svb_graph_begin(void* stream) {
+  return guard([&] { SVB_CUDA_TRY(cudaStreamBeginCapture(S(stream), cudaStreamCaptureModeThreadLocal)); });
+}
+int svb_graph_end(void* stream, void** out) {
+  return guard([&] {
+    cudaGraph_t g = nullptr;
+    SVB_CUDA_TRY(cudaStreamEndCapture(S(stream), &g));
+    auto* h = new svb_graph();
+    size_t nn = 0;
+    SVB_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) SVB_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      SVB_CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+      h->kernels += t == cudaGraphNodeTypeKernel;
+    }
+    const cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      delete h;
+      SVB_CUDA_TRY(e);
+    }
+    // the captured launches were counted once at capture time; replays count again
+    note_launches(-h->kernels);
+    *out = h;
+  });
+}
+int svb_graph_launch(void* graph, void* stream) {
+  return guard([&] {
+    auto* h = static_cast<svb_graph*>(graph);
+    SVB_CUDA_TRY(cudaGraphLaunch(h->exec, S(stream)));
+    note_launches(h->kernels);
+  });
+}
+int svb_graph_destroy(void* graph) {
+  return guard([&] {
+    auto* h = static_cast<svb_graph*>(graph);
+    if (h && h->exec) cudaGraphExecDestroy(h->exec);
+    delete h;
+  });
+}
+
 int svb_event_record(void* stream, void** out) {
   return guard([&] {
     cudaEvent_t e;

@@ -1,6 +1,6 @@
 """Profiling driver: a few launches of one SpMV configuration on one of the
 sweep matrices (for ncu).  python profiles/run_spmv.py <matrix> <token> [reps]
-matrix: poisson1024 | convdiff2000 | powerlaw2M"""
+matrix: poisson1024 | convdiff2000 | powerlaw2M | powerlaw8M"""
 import sys
 from pathlib import Path
 
@@ -24,6 +24,8 @@ elif name == "convdiff2000":
             offs.append((dy, dx))
             w.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
     A = P.CsrMatrix.stencil((2000, 2000), offs, w)
+elif name == "powerlaw8M":
+    A = P.CsrMatrix(*G.powerlaw_spd(8_000_000, seed=0))
 else:
     A = P.CsrMatrix(*G.powerlaw_spd(2_000_000, seed=0))
 cfg = P.SpmvConfig.from_token(tok)
