@@ -279,3 +279,24 @@ def test_time_config_and_compare():
     cmp = P.compare_solvers(E, P.GmresParams(tol=1e-10), stub_cascade(fmt="DIA"), matrix_id="eye4")
     for r in (cmp.default, cmp.sequential, cmp.async_):
         assert r.converged and r.iterations == 1
+
+
+def test_cg_graph_batches_match_uncaptured():
+    """CG batches replayed as CUDA graphs give the same iterations, history
+    and solution as the uncaptured batches (same kernels, same order)."""
+    import paper_2411_10143_b200 as P
+    from paper_2411_10143_b200 import generators as G, solver
+    A = P.CsrMatrix(*G.poisson2d(96))
+    params = P.GmresParams(tol=1e-8, max_iters=4000)
+    cfg = P.SpmvConfig.from_token("DIA/LibA")
+    old = solver._CG_GRAPHS
+    try:
+        solver._CG_GRAPHS = True
+        r1 = P.cg_solve(A, None, params, initial_config=cfg)
+        solver._CG_GRAPHS = False
+        r2 = P.cg_solve(A, None, params, initial_config=cfg)
+    finally:
+        solver._CG_GRAPHS = old
+    assert r1.iterations == r2.iterations > 64        # several full (captured) batches ran
+    assert r1.residual_history == r2.residual_history
+    assert np.array_equal(r1.solution, r2.solution)
