@@ -23,7 +23,9 @@ ds = Path(sys.argv[1])
 rows = [ln for ln in (ds / "FORMAT.csv").read_text().splitlines()[2:]]
 cache = {json.loads(f.read_text())["matrix_id"]: json.loads(f.read_text())["times"]
          for f in (ds / "cache").glob("*.json")}
-ids = sorted(cache)
+ids = list(cache)
+ids = sorted(ids, key=lambda i: int(i.rsplit("_", 1)[-1])) if all(
+    i.rsplit("_", 1)[-1].isdigit() for i in ids) else sorted(ids)
 assert len(ids) == len(rows)
 sets = {"default CSR/LibA/32": None}
 for d in sys.argv[2:]:

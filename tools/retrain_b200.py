@@ -26,6 +26,15 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
+def dataset_order(ids):
+    """Row order of build_dataset's CSVs: generation order for a generated
+    corpus (ids end in _<index>), file-name order for a .mtx directory."""
+    ids = list(ids)
+    if ids and all(i.rsplit("_", 1)[-1].isdigit() for i in ids):
+        return sorted(ids, key=lambda i: int(i.rsplit("_", 1)[-1]))
+    return sorted(ids)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("dataset")
@@ -75,7 +84,7 @@ def main():
     prov = {"dataset": str(ds), "tie": args.tie, "trees": args.trees, "depth": args.depth, "models": {}}
     fp = (ds / "FORMAT.csv").read_text().splitlines()[0]
     prov["fingerprint"] = fp
-    ids_in_order = sorted(cache)          # generated ids sort in generation order
+    ids_in_order = dataset_order(cache)
     routes = {name: [] for name in DATASET_FILES}
     from paper_2411_10143_b200.harness import route_labels
     for mid in ids_in_order:
