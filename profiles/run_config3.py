@@ -24,10 +24,12 @@ nr, nc, ptr, cols, vals = G.powerlaw_spd(n, seed=0)
 gen_s = time.perf_counter() - t0
 A = P.CsrMatrix(nr, nc, ptr, cols, vals)
 A._device()
-models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
+import os  # noqa: E402
+models = P.CascadeModelSet.load_dir(P.B200_MODELS_DIR if os.environ.get("MODELS") == "b200"
+                                    else ROOT / "tests" / "golden" / "models")
 params = P.GmresParams(tol=1e-8, max_iters=20000, rhs="random", seed=0)
 start = P.GPU_DEFAULT_CONFIG
-out = {"workload": f"config3: CG fp64 power-law SPD n={nr:,} nnz={A.nnz:,}, b random seed 0, tol 1e-8",
+out = {"models": os.environ.get("MODELS", "shipped"), "workload": f"config3: CG fp64 power-law SPD n={nr:,} nnz={A.nnz:,}, b random seed 0, tol 1e-8",
        "host_generation_s": gen_s}
 fv = P.extract_features(A)
 out["features"] = {k: getattr(fv, k) for k in ("mean", "sd", "cov", "max", "ndiag", "diagfill")}
