@@ -98,6 +98,7 @@ int svb_stream_create(int priority, void** out);   /* non-blocking stream */
 int svb_stream_destroy(void* stream);
 int svb_event_record(void* stream, void** out);    /* new event, recorded on stream */
 int svb_event_query(void* event);                  /* SVB_OK when complete, else SVB_INVALID */
+int svb_event_sync(void* event);                   /* block until the event completes */
 int svb_stream_wait_event(void* stream, void* event);
 int svb_event_destroy(void* event);
 /* CUDA graph capture of work enqueued on `stream` by this thread (B200
@@ -261,6 +262,14 @@ int svb_vec_axpby(svb_vecops* v, double a, const double* x_dev, double b, double
                   void* stream);
 /* x *= s */
 int svb_vec_scale(svb_vecops* v, double* x_dev, double s, void* stream);
+/* Row-partitioned CG on device scalars sc[] (NCCL all-reduces them in place
+ * between calls): x += a p, r -= a q, a = sc[irr]/sc[ipq], local r.r ->
+ * sc[out] (a zero/non-finite sc[ipq] leaves x, r untouched); then
+ * p = r + (sc[inew]/sc[iold]) p.  Oracle: oracle/cpu_oracle.py:cg. */
+int svb_dcg_update(svb_vecops* v, double* sc_dev, int32_t irr, int32_t ipq, int32_t out, const double* p_dev,
+                   const double* q_dev, double* x_dev, double* r_dev, void* stream);
+int svb_dcg_p(svb_vecops* v, const double* sc_dev, int32_t inew, int32_t iold, const double* r_dev,
+              double* p_dev, void* stream);
 /* x[0..n) = v on the device (row-partitioned setup: windows of ones) */
 int svb_fill(double* x_dev, int64_t n, double v, void* stream);
 

@@ -75,6 +75,9 @@ _SIGS = {
     "svb_matrix_download": [_P, C.c_int, _P, _P],
     "svb_csr_stencil": [C.c_int, _PI64, C.c_int, C.POINTER(C.c_int32), _PD, _P, _PP],
     "svb_fill": [_P, C.c_int64, C.c_double, _P],
+    "svb_event_sync": [_P],
+    "svb_dcg_update": [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],
+    "svb_dcg_p": [_P, _P, C.c_int32, C.c_int32, _P, _P, _P],
     "svb_krylov_mark": [_P, _P],
     "svb_graph_begin": [_P],
     "svb_graph_end": [_P, _PP],

@@ -908,6 +908,53 @@ __global__ void __launch_bounds__(KB) k_dot(int64_t n, const double* __restrict_
   if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = tot;
 }
 
+// Row-partitioned CG, fused on device scalars sc[] (all-reduced in place
+// between the kernels): x += a p, r -= a q with a = sc[irr]/sc[ipq], and the
+// local r.r into sc[out].  A zero or non-finite p.Ap leaves x and r untouched
+// (the host then confirms with the true residual or reports the breakdown,
+// as in the unfused loop) and copies r.r through unchanged.
+__global__ void __launch_bounds__(KB) k_dcg_update(int64_t n, double* sc, int irr, int ipq, int out,
+                                                   const double* __restrict__ p, const double* __restrict__ q,
+                                                   double* __restrict__ x, double* __restrict__ r, double* partials,
+                                                   unsigned* counter) {
+  const double pq = sc[ipq];
+  const bool ok = pq != 0.0 && isfinite(pq);
+  const double a = ok ? sc[irr] / pq : 0.0;
+  double acc = 0.0;
+  if (ok) {
+    for_pairs(
+        n,
+        [&](int64_t e) {
+          const double2 pp = ld2(p + e), qq = ld2(q + e), xx = ld2(x + e), rr = ld2(r + e);
+          const double2 rn = make_double2(rr.x - a * qq.x, rr.y - a * qq.y);
+          st2(x + e, make_double2(xx.x + a * pp.x, xx.y + a * pp.y));
+          st2(r + e, rn);
+          acc += rn.x * rn.x + rn.y * rn.y;
+        },
+        [&](int64_t e) {
+          x[e] = x[e] + a * p[e];
+          const double rn = r[e] - a * q[e];
+          r[e] = rn;
+          acc += rn * rn;
+        });
+  }
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) sc[out] = ok ? tot : sc[irr];
+}
+
+// p = r + b p with b = sc[inew]/sc[iold]
+__global__ void __launch_bounds__(KB) k_dcg_p(int64_t n, const double* sc, int inew, int iold,
+                                              const double* __restrict__ r, double* __restrict__ p) {
+  const double b = sc[inew] / sc[iold];
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        const double2 rr = ld2(r + e), pp = ld2(p + e);
+        st2(p + e, make_double2(rr.x + b * pp.x, rr.y + b * pp.y));
+      },
+      [&](int64_t e) { p[e] = r[e] + b * p[e]; });
+}
+
 __global__ void __launch_bounds__(KB) k_fill(double* __restrict__ x, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
@@ -1300,6 +1347,23 @@ int svb_vec_axpy_dot(svb_vecops* v, const double* alpha, double sign, const doub
   return guard([&] {
     k_axpy_dot<<<v->grid, KB, 0, S(stream)>>>(v->n, alpha, sign, x, y, z, ptr<double>(v->partials), vctr(v),
                                                out);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_dcg_update(svb_vecops* v, double* sc, int32_t irr, int32_t ipq, int32_t out, const double* p,
+                   const double* q, double* x, double* r, void* stream) {
+  return guard([&] {
+    k_dcg_update<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, irr, ipq, out, p, q, x, r, ptr<double>(v->partials),
+                                                 vctr(v));
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_dcg_p(svb_vecops* v, const double* sc, int32_t inew, int32_t iold, const double* r, double* p,
+              void* stream) {
+  return guard([&] {
+    k_dcg_p<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, inew, iold, r, p);
     SVB_CHECK_LAUNCH();
   });
 }

@@ -304,6 +304,9 @@ int svb_event_record(void* stream, void** out) {
     *out = e;
   });
 }
+int svb_event_sync(void* event) {
+  return guard([&] { SVB_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(event))); });
+}
 int svb_event_query(void* event) {
   cudaError_t e = cudaEventQuery(reinterpret_cast<cudaEvent_t>(event));
   if (e == cudaSuccess) return SVB_OK;

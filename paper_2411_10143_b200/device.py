@@ -52,6 +52,9 @@ class Event:
         _lib.check(_lib.lib().svb_event_record(stream.handle if stream else None, ctypes.byref(h)))
         self.handle = h.value
 
+    def sync(self):
+        _lib.check(_lib.lib().svb_event_sync(self.handle))
+
     def done(self) -> bool:
         st = _lib.lib().svb_event_query(self.handle)
         if st == _lib.OK:

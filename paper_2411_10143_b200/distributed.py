@@ -271,6 +271,28 @@ class CudaOps:
     def scale(self, x, s: float):
         _lib.check(self.L.svb_vec_scale(self.h, x.ptr, s, self.stream.handle))
 
+    def cg_update(self, sc, irr: int, ipq: int, out: int, p, q, x, r):
+        _lib.check(self.L.svb_dcg_update(self.h, sc.ptr, irr, ipq, out, p.ptr, q.ptr, x.ptr, r.ptr,
+                                         self.stream.handle))
+
+    def cg_p(self, sc, inew: int, iold: int, r, p):
+        _lib.check(self.L.svb_dcg_p(self.h, sc.ptr, inew, iold, r.ptr, p.ptr, self.stream.handle))
+
+    def read_async(self, sc, count: int):
+        """Copy sc[:count] into pinned host memory behind the work enqueued so
+        far; read_wait() returns it.  The stream keeps running meanwhile."""
+        if getattr(self, "_pin", None) is None:
+            h = ctypes.c_void_p()
+            _lib.check(self.L.svb_host_alloc(64 * 8, ctypes.byref(h)))
+            self._pin = h.value
+        device.copy(self._pin, sc.ptr, 8 * count, self.stream)
+        return (self.stream.record(), count)
+
+    def read_wait(self, token) -> np.ndarray:
+        ev, count = token
+        ev.sync()
+        return np.ctypeslib.as_array((ctypes.c_double * count).from_address(self._pin)).copy()
+
     def spmv(self, mat, cfg: SpmvConfig, window, dst):
         launch(cfg, mat, window.ptr, dst.ptr, workers=default_workers(), stream=self.stream)
 
@@ -484,15 +506,20 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
 
 def dist_cg(A: DistOperator, b_local, params) -> dict:
     """Hestenes-Stiefel CG over row-partitioned vectors (oracle/cpu_oracle.py:
-    cg): one halo exchange + local SpMV and two scalar all-reduces per
-    iteration."""
+    cg).  Per iteration: one halo exchange + local SpMV, a local p.Ap and a
+    fused x/r update with r.r (svb_dcg_update) on device scalars, each
+    followed by an in-place scalar all-reduce, then p = r + beta p
+    (svb_dcg_p).  The host reads (p.Ap, r.r) through pinned memory after the
+    p update is already enqueued, so the GPU keeps working while the host
+    runs the convergence test; a breakdown (p.Ap = 0) leaves x and r
+    untouched, exactly as the unfused loop."""
     ops, comm = A.ops, A.comm
     x, r, q, bvec = ops.vec(), ops.vec(), ops.vec(), ops.vec()
     p = ops.vec() if A.no_halo else A.own_view()   # p lives in the halo window
     ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
         ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
-    sc = ops.scalars(4)
-    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 0))
+    sc = ops.scalars(6)            # [rr_a, rr_b, p.Ap, ||b||^2, true residual, -]
+    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 3))
     hist, done = [], 0
 
     def out(conv, fin, status="ok"):
@@ -503,7 +530,7 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
         A.apply(x, q)
         ops.axpby(1.0, bvec, -1.0, q)
         ops.axpby(1.0, q, 0.0, r)
-        return math.sqrt(_global_norm2(ops, comm, r, sc, 1)) / bnorm
+        return math.sqrt(_global_norm2(ops, comm, r, sc, 4)) / bnorm
 
     if bnorm == 0.0:
         if params.max_iters >= 1:
@@ -513,12 +540,18 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
         return out(False, None)
     ops.axpby(1.0, bvec, 0.0, r)
     ops.axpby(1.0, r, 0.0, p)
-    rr = _global_norm2(ops, comm, r, sc, 2)
+    cur, nxt = 0, 1
+    _global_norm2(ops, comm, r, sc, cur)
     while done < params.max_iters:
         A.apply(p, q)
-        ops.dot(p, q, sc, 3)
-        comm.allreduce(sc, 3, 1)
-        pq = float(ops.read(sc, 4)[3])
+        ops.dot(p, q, sc, 2)
+        comm.allreduce(sc, 2, 1)
+        ops.cg_update(sc, cur, 2, nxt, p, q, x, r)
+        comm.allreduce(sc, nxt, 1)
+        tok = ops.read_async(sc, 3)
+        ops.cg_p(sc, nxt, cur, r, p)         # speculative: unused if the loop stops here
+        vals = ops.read_wait(tok)
+        pq, rr_new = float(vals[2]), float(vals[nxt])
         _finite(pq, "curvature p.Ap", done + 1)
         if pq == 0.0:
             fin = true_res()
@@ -526,23 +559,18 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
                 return out(True, fin)
             raise StagnationError(f"CG breakdown (p.Ap = 0) at iteration {done + 1} with relative "
                                   f"residual {fin:.3e} above tol {params.tol:.3e}")
-        alpha = rr / pq
-        ops.axpby(alpha, p, 1.0, x)
-        ops.axpby(-alpha, q, 1.0, r)
-        rr_new = _global_norm2(ops, comm, r, sc, 2)
         done += 1
         est = math.sqrt(rr_new) / bnorm
         _finite(est, "residual estimate", done)
         hist.append(est)
+        cur, nxt = nxt, cur
         if est <= params.tol:
             fin = true_res()                      # leaves r = b - A x
             if fin <= params.tol:
                 return out(True, fin)
             ops.axpby(1.0, r, 0.0, p)
-            rr = _global_norm2(ops, comm, r, sc, 2)
+            _global_norm2(ops, comm, r, sc, cur)
             continue
-        ops.axpby(1.0, r, rr_new / rr, p)
-        rr = rr_new
     fin = true_res()
     return out(fin <= params.tol, fin)
 

@@ -59,6 +59,25 @@ class NumpyOps:
     def axpby(self, a, x, b, y):
         y[:] = a * x + b * y
 
+    def cg_update(self, sc, irr, ipq, out, p, q, x, r):
+        pq = sc[ipq]
+        if pq == 0.0 or not np.isfinite(pq):
+            sc[out] = sc[irr]
+            return
+        a = sc[irr] / pq
+        x += a * p
+        r -= a * q
+        sc[out] = float(np.dot(r, r))
+
+    def cg_p(self, sc, inew, iold, r, p):
+        p[:] = r + (sc[inew] / sc[iold]) * p
+
+    def read_async(self, sc, count):
+        return sc[:count].copy()
+
+    def read_wait(self, token):
+        return token
+
     def scale(self, x, s):
         x *= s
 
