@@ -921,7 +921,17 @@ __global__ void __launch_bounds__(KB) k_dcg_update(int64_t n, double* sc, int ir
   const bool ok = pq != 0.0 && isfinite(pq);
   const double a = ok ? sc[irr] / pq : 0.0;
   double acc = 0.0;
-  if (ok) {
+  // p may be a slice of a halo window at an odd element offset: pairs only
+  // when every operand is 16-byte aligned
+  const bool al = (((uintptr_t)p | (uintptr_t)q | (uintptr_t)x | (uintptr_t)r) & 15) == 0;
+  if (ok && !al) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+      x[e] = x[e] + a * p[e];
+      const double rn = r[e] - a * q[e];
+      r[e] = rn;
+      acc += rn * rn;
+    }
+  } else if (ok) {
     for_pairs(
         n,
         [&](int64_t e) {
@@ -946,6 +956,11 @@ __global__ void __launch_bounds__(KB) k_dcg_update(int64_t n, double* sc, int ir
 __global__ void __launch_bounds__(KB) k_dcg_p(int64_t n, const double* sc, int inew, int iold,
                                               const double* __restrict__ r, double* __restrict__ p) {
   const double b = sc[inew] / sc[iold];
+  if ((((uintptr_t)r | (uintptr_t)p) & 15) != 0) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+      p[e] = r[e] + b * p[e];
+    return;
+  }
   for_pairs(
       n,
       [&](int64_t e) {

@@ -38,7 +38,7 @@ from .formats import CsrMatrix, FormatTag, convert
 from .kernels import Library, SpmvConfig, default_workers, launch
 
 __all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
-           "NcclComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
+           "NcclComm", "HostStagedComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
            "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve"]
 
 
@@ -346,6 +346,57 @@ class NcclComm:
                 w.wait()
 
 
+class HostStagedComm:
+    """The same collectives over gloo with device buffers staged through the
+    host.  Not a production path: it lets the CUDA implementation (CudaOps,
+    device halo windows, device scalars) run with several ranks on ONE GPU
+    (NCCL refuses two ranks per device), which is how the test suite covers
+    world size > 1 of the CUDA path on a single-GPU box."""
+
+    def __init__(self, stream: device.Stream):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.stream = torch, dist, stream
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def _down(self, ptr: int, n: int) -> np.ndarray:
+        a = np.empty(n)
+        if n:
+            device.copy(a.ctypes.data, ptr, 8 * n, self.stream)
+            self.stream.sync()
+        return a
+
+    def _up(self, ptr: int, a: np.ndarray):
+        if a.size:
+            device.copy(ptr, a.ctypes.data, a.nbytes, self.stream)
+            self.stream.sync()
+
+    def allreduce(self, sc, first: int, count: int):
+        a = self._down(sc.ptr + 8 * first, count)
+        t = self.torch.from_numpy(a)
+        self.dist.all_reduce(t)
+        self._up(sc.ptr + 8 * first, a)
+
+    def allreduce_max(self, arr: np.ndarray) -> np.ndarray:
+        t = self.torch.from_numpy(np.asarray(arr, dtype=np.float64).copy())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.numpy()
+
+    def allgather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def exchange(self, sends, recvs):
+        reqs = [self.dist.isend(self.torch.from_numpy(self._down(v.ptr, v.n)), p) for p, v in sends]
+        bufs = [(v, self.torch.zeros(v.n, dtype=self.torch.float64)) for _, v in recvs]
+        reqs += [self.dist.irecv(t, p) for (p, _), (_, t) in zip(recvs, bufs)]
+        for r in reqs:
+            r.wait()
+        for v, t in bufs:
+            self._up(v.ptr, t.numpy())
+
+
 # ---------------------------------------------------------------------------
 # distributed operator: halo exchange + local SpMV
 # ---------------------------------------------------------------------------
@@ -596,7 +647,7 @@ def global_features(block: LocalBlock, nrows: int, ncols: int, nnz: int, comm, l
 
 def distributed_stencil_solve(method: str, dims, offsets, weights, params, models=None,
                               initial_config: SpmvConfig | None = None, blk: "LocalBlock | None" = None,
-                              timings: dict | None = None):
+                              timings: dict | None = None, comm_class=None):
     """Row-partitioned solve of a device-generated stencil matrix under
     torchrun (NCCL), b = A*1 (solver.py:188-193).  Each rank generates its
     z-slab on its own GPU (or reuses ``blk``); with ``models`` the cascade
@@ -612,7 +663,7 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
     if blk is None:
         blk = stencil_block(dims, offsets, weights, r0, r1, stream)
     n = blk.ncols_global
-    ops, comm = CudaOps(blk.nloc, stream), NcclComm(stream)
+    ops, comm = CudaOps(blk.nloc, stream), (comm_class or NcclComm)(stream)
     csr = ops.local_csr(blk)
     # b = A * 1 on this rank's rows (a window of ones times the local rows),
     # outside the clock as in the reference (solver.py:355-358)

@@ -105,3 +105,79 @@ def test_distributed_stencil_solve_world1(nccl_world1, method, dims):
     fv = P.extract_features(P.CsrMatrix(n, n, ptr, cols, vals))
     assert res["config"] == P.cascade_predict(models, fv).token()
     assert t["total_s"] > 0
+
+
+def _world2_worker(rank, port, method, dims, q):
+    """One of two ranks sharing the single test GPU: CUDA kernels, device
+    halo windows and device scalars, collectives staged through gloo."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2411_10143_b200.distributed import HostStagedComm, distributed_stencil_solve
+        offs, w = _stencil(dims)
+        params = P.GmresParams(restart_m=30, tol=1e-8, max_iters=3000)
+        models = P.CascadeModelSet.load_dir(os.path.join(os.path.dirname(__file__), "golden", "models"))
+        res, blk = distributed_stencil_solve(method, dims, offs, w, params, models=models,
+                                             comm_class=HostStagedComm)
+        q.put((rank, blk.r0, blk.r1, res["iterations"], res["converged"], res["final"],
+               res["x"].to_numpy(), res["config"], blk.cmin, blk.cmax))
+    except Exception as exc:          # surface worker failures in the parent
+        import traceback
+        q.put((rank, "error", repr(exc) + traceback.format_exc()[-1500:]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _stencil(dims):
+    if len(dims) == 3:
+        offs, w = [], []
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    offs.append((dz, dy, dx))
+                    w.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+        return offs, w
+    offs = [(dy, dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    return offs, [8.5 if o == (0, 0) else -1.0 - 0.25 * (o[1] + o[0]) for o in offs]
+
+
+@pytest.mark.parametrize("method,dims", [("cg", (14, 12, 10)), ("gmres", (44, 40))])
+def test_cuda_path_world2_on_one_gpu(method, dims):
+    """World size 2 of the CUDA row-partitioned path (two processes on the
+    one GPU, gloo-staged collectives): the halo exchange really moves planes
+    between ranks; iterations within 1 of the oracle and the assembled x
+    matches it."""
+    import multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_world2_worker, args=(r, port, method, dims, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    errors = [o for o in out if o[1] == "error"]
+    assert not errors, errors
+    offs, w = _stencil(dims)
+    n, _, ptr, cols, vals = G.stencil_csr(dims, offs, w)
+    csr = O.OCsr(n, n, ptr, cols, vals)
+    b = O.spmv_sequential(csr, np.ones(n))
+    mv = lambda v: O.spmv("CSR/LibB", csr, v)      # noqa: E731
+    ref = O.cg(mv, b, tol=1e-8, max_iters=3000) if method == "cg" else \
+        O.gmres(mv, b, restart=30, tol=1e-8, max_iters=3000)
+    (_, a0, a1, it0, c0, f0, x0, cfg0, _, cmax0), (_, b0, b1, it1, c1, f1, x1, cfg1, cmin1, _) = out
+    assert a0 == 0 and a1 == b0 and b1 == n and cmax0 >= a1 and cmin1 < b0   # real halos both ways
+    assert it0 == it1 and c0 and c1 and f0 == f1 and f0 <= 1e-8
+    assert abs(it0 - ref["iterations"]) <= 1
+    x = np.concatenate([x0, x1])
+    assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+    fv = P.extract_features(P.CsrMatrix(n, n, ptr, cols, vals))
+    assert cfg0 == cfg1 == P.cascade_predict(
+        P.CascadeModelSet.load_dir(os.path.join(os.path.dirname(__file__), "golden", "models")), fv).token()
