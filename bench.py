@@ -493,15 +493,21 @@ def b200_arm(args):
     detail = {}
     if rank == 0:
         with DeviceOptions(keep_solution_on_device=True):
-            t0 = time.perf_counter()
-            d = P.gmres_solve(A, b_dev, params, initial_config=start_cfg)
-            torch.cuda.synchronize()
-            detail["default_csr_vector_gpu_s"] = time.perf_counter() - t0
+            def timed(fn, reps=3):          # median of `reps` warm runs
+                ts, rep = [], None
+                for _ in range(reps):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    rep = fn()
+                    torch.cuda.synchronize()
+                    ts.append(time.perf_counter() - t0)
+                    rep.solution = None
+                return statistics.median(ts), rep
+            dt, d = timed(lambda: P.gmres_solve(A, b_dev, params, initial_config=start_cfg))
+            detail["default_csr_vector_gpu_s"] = dt
             detail["default_iterations"] = d.iterations
-            t0 = time.perf_counter()
-            sq = P.sequential_predict_solve(A, b_dev, params, models)
-            torch.cuda.synchronize()
-            detail["sequential_gpu_s"] = time.perf_counter() - t0
+            st, sq = timed(lambda: P.sequential_predict_solve(A, b_dev, params, models))
+            detail["sequential_gpu_s"] = st
             detail["sequential_phases"] = sq.phases
         if not args.no_extra:
             detail["config1_cg"] = config1_cg(P, device, _lib, models, start_cfg)
