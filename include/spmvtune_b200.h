@@ -48,7 +48,8 @@ typedef enum {
   SVB_NONFINITE = 4,
   SVB_OOM = 5,
   SVB_CUDA = 6,
-  SVB_INVALID = 7
+  SVB_INVALID = 7,
+  SVB_FORMAT_ERROR = 8   /* -> MatrixMarketError */
 } svb_status;
 
 /* FormatTag (formats.py:21-26) */
@@ -155,6 +156,22 @@ int svb_csr_stencil(int ndim, const int64_t* dims, int nst, const int32_t* offse
 int svb_csr_stencil_rows(int ndim, const int64_t* dims, int nst, const int32_t* offsets,
                          const double* weights, int64_t r0, int64_t r1, int64_t cmin, int64_t cmax,
                          void* stream, svb_matrix** out);
+
+/* ---- Matrix Market ingest (mmio.py:32-126) + from_triplets on the device
+ * (formats.py:86-100).  svb_mm_open reads the file and validates banner and
+ * size line (dims = {nrows, ncols, nnz}, flags = {pattern, symmetric});
+ * svb_mm_parse fills caller-owned 0-based rows/cols/vals[nnz] with nthreads
+ * host threads (0 = all cores), reporting the lowest failing entry with the
+ * reference's message; status SVB_FORMAT_ERROR maps to MatrixMarketError.
+ * svb_coo_from_triplets sorts (stable radix sort on the device) and, with
+ * sum_duplicates, merges repeated coordinates in np.add.reduceat order. */
+typedef struct svb_mm svb_mm;
+int svb_mm_open(const char* path, int64_t* dims, int32_t* flags, svb_mm** out);
+int svb_mm_parse(svb_mm* h, int64_t* rows_host, int64_t* cols_host, double* vals_host, int32_t nthreads);
+int svb_mm_close(svb_mm* h);
+int svb_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, const int64_t* rows_host,
+                          const int64_t* cols_host, const double* vals_host, int32_t sum_duplicates,
+                          void* stream, svb_matrix** out);
 
 /* ---- conversion: convert(m, target) (formats.py:302-320) ----------------
  * Bit-exact with the reference arrays.  DIA above 4096 diagonals returns

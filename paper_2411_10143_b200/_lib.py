@@ -12,12 +12,12 @@ import os
 import threading
 from pathlib import Path
 
-from .errors import (FormatInapplicableError, SolverNumericalError,
+from .errors import (FormatInapplicableError, MatrixMarketError, SolverNumericalError,
                      UnsupportedConfigError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libspmvtune_b200.so"
 
-OK, UNSUPPORTED, INAPPLICABLE, DIM_MISMATCH, NONFINITE, OOM, CUDA, INVALID = range(8)
+OK, UNSUPPORTED, INAPPLICABLE, DIM_MISMATCH, NONFINITE, OOM, CUDA, INVALID, FORMAT_ERROR = range(9)
 COO, CSR, ELL, DIA, HYB = range(5)
 LIBA, LIBB, LIBC = range(3)
 F64, F32 = 0, 1
@@ -75,6 +75,10 @@ _SIGS = {
     "svb_matrix_download": [_P, C.c_int, _P, _P],
     "svb_csr_stencil": [C.c_int, _PI64, C.c_int, C.POINTER(C.c_int32), _PD, _P, _PP],
     "svb_fill": [_P, C.c_int64, C.c_double, _P],
+    "svb_mm_open": [C.c_char_p, _PI64, C.POINTER(C.c_int32), _PP],
+    "svb_mm_parse": [_P, _P, _P, _P, C.c_int32],
+    "svb_mm_close": [_P],
+    "svb_coo_from_triplets": [C.c_int64, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, _PP],
     "svb_event_sync": [_P],
     "svb_dcg_update": [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],
     "svb_dcg_p": [_P, _P, C.c_int32, C.c_int32, _P, _P, _P],
@@ -177,7 +181,7 @@ def last_error() -> str:
 
 _EXC = {UNSUPPORTED: UnsupportedConfigError, INAPPLICABLE: FormatInapplicableError,
         DIM_MISMATCH: ValueError, NONFINITE: SolverNumericalError, OOM: MemoryError,
-        CUDA: RuntimeError, INVALID: ValueError}
+        CUDA: RuntimeError, INVALID: ValueError, FORMAT_ERROR: MatrixMarketError}
 
 
 def check(status: int) -> None:

@@ -35,6 +35,7 @@ SOURCES = {
     "krylov.cu": [],
     "generate.cu": [],
     "forest.cpp": [],
+    "mmio.cu": [],
 }
 
 
