@@ -255,6 +255,9 @@ int svb_cg_step(svb_krylov* k, double bnorm, void* stream);
 int svb_cg_batch_reset(svb_krylov* k, double tol, int64_t history_cap, void* stream);
 int svb_cg_batch_resume(svb_krylov* k, void* stream);   /* clear `done`, keep count */
 int svb_cg_step_batched(svb_krylov* k, double bnorm, void* stream);
+/* One batched CG iteration for a DIA operator with q = A p fused with p.q
+ * (same q as svb_spmv DIA/LibA; saves the separate p.q pass). */
+int svb_cg_step_batched_dia(svb_krylov* k, const svb_matrix* dia, double bnorm, void* stream);
 int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, void* stream);
 
 /* ---- generic fused vector ops (device vectors of length n) -------------- */

@@ -16,6 +16,8 @@ from .errors import (FormatInapplicableError, MatrixMarketError, SolverNumerical
                      UnsupportedConfigError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libspmvtune_b200.so"
+if os.environ.get("SPMVTUNE_LIB_VARIANT"):        # A/B experiments on kernel variants
+    LIB_PATH = LIB_PATH.with_name(f"libspmvtune_b200_{os.environ['SPMVTUNE_LIB_VARIANT']}.so")
 
 OK, UNSUPPORTED, INAPPLICABLE, DIM_MISMATCH, NONFINITE, OOM, CUDA, INVALID, FORMAT_ERROR = range(9)
 COO, CSR, ELL, DIA, HYB = range(5)
@@ -82,6 +84,7 @@ _SIGS = {
     "svb_event_sync": [_P],
     "svb_dcg_update": [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],
     "svb_dcg_p": [_P, _P, C.c_int32, C.c_int32, _P, _P, _P],
+    "svb_cg_step_batched_dia": [_P, _P, C.c_double, _P],
     "svb_krylov_mark": [_P, _P],
     "svb_graph_begin": [_P],
     "svb_graph_end": [_P, _PP],

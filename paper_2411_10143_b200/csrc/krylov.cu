@@ -46,6 +46,8 @@ struct svb_krylov {
   // next SpMV, CG's p update) overlaps the host's decision
   cudaEvent_t ev = nullptr;
   svb::Buf ctl, hist;   // batched-CG control block and estimate log
+  unsigned dgrid = 1;
+  svb::Buf dparts;      // fused DIA SpMV+dot partials (dgrid doubles + counter)
   int64_t hist_cap = 0;
   ~svb_krylov() {
     if (ev) cudaEventDestroy(ev);
@@ -738,6 +740,8 @@ __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restr
 // ---------------------------------------------------------------------------
 // CG
 // ---------------------------------------------------------------------------
+enum { S_PQ = 3 };   // scal slot of the fused SpMV+dot result
+
 // r = b - tmp; p = r; rr = r.r
 __global__ void __launch_bounds__(KB) k_cg_restart(int64_t n, const double* __restrict__ b,
                                                    const double* __restrict__ t, double* __restrict__ r,
@@ -780,6 +784,25 @@ struct CgCtl {
   double* hist;   // per-iteration residual estimates
 };
 enum { CG_RUN = 0, CG_TOL = 1, CG_PQ0 = 2, CG_NONFINITE = 3 };
+
+// r.r of the updated residual -> beta, rr, estimate, history, stop flags
+__device__ __forceinline__ void cg_after_update(double* scal, double tot, double bnorm, svb_krylov_status* st,
+                                                CgCtl* ctl) {
+  const double rr_old = scal[S_RR];
+  scal[S_BETA] = tot / rr_old;
+  scal[S_RR] = tot;
+  const double est = sqrt(tot) / bnorm;
+  st->estimate = est;
+  st->nonfinite = st->nonfinite || bad(tot) || bad(est);
+  if (ctl != nullptr) {
+    if (ctl->count < ctl->cap) ctl->hist[ctl->count] = est;
+    ctl->count += 1;
+    st->count = ctl->count;
+    if (bad(tot) || bad(est)) ctl->done = CG_NONFINITE;
+    else if (est <= ctl->tol) ctl->done = CG_TOL;
+    st->done = ctl->done;
+  }
+}
 
 // alpha = rr / (p.q)
 __global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restrict__ p,
@@ -835,25 +858,51 @@ __global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict_
         acc += rr * rr;
       });
   double tot;
-  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
-    const double rr_old = scal[S_RR];
-    scal[S_BETA] = tot / rr_old;
-    scal[S_RR] = tot;
-    const double est = sqrt(tot) / bnorm;
-    st->estimate = est;
-    st->nonfinite = st->nonfinite || bad(tot) || bad(est);
-    if (ctl != nullptr) {
-      if (ctl->count < ctl->cap) ctl->hist[ctl->count] = est;
-      ctl->count += 1;
-      st->count = ctl->count;
-      if (bad(tot) || bad(est)) ctl->done = CG_NONFINITE;
-      else if (est <= ctl->tol) ctl->done = CG_TOL;
-      st->done = ctl->done;
-    }
-  }
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) cg_after_update(scal, tot, bnorm, st, ctl);
 }
 
 // p = r + beta p
+__global__ void __launch_bounds__(KB) k_cg_update_pq(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                     const double* __restrict__ p, const double* __restrict__ q,
+                                                     double* scal, double bnorm, double* partials,
+                                                     unsigned* counter, svb_krylov_status* st, CgCtl* ctl) {
+  if (ctl->done) return;
+  const double pq = scal[S_PQ];
+  if (bad(pq) || pq == 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pq = pq;
+      st->nonfinite = bad(pq);
+      ctl->done = bad(pq) ? CG_NONFINITE : CG_PQ0;
+      st->done = ctl->done;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->pq = pq;
+  const double alpha = scal[S_RR] / pq;
+  double acc = 0.0;
+  for_pairs(
+      n,
+      [&](int64_t e) {
+        double2 xx = ld2(x + e), rr = ld2(r + e), pp = ld2(p + e), qq = ld2(q + e);
+        xx.x += alpha * pp.x;
+        xx.y += alpha * pp.y;
+        rr.x -= alpha * qq.x;
+        rr.y -= alpha * qq.y;
+        st2(x + e, xx);
+        st2(r + e, rr);
+        acc += rr.x * rr.x;
+        acc += rr.y * rr.y;
+      },
+      [&](int64_t e) {
+        x[e] += alpha * p[e];
+        double rr = r[e] - alpha * q[e];
+        r[e] = rr;
+        acc += rr * rr;
+      });
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) cg_after_update(scal, tot, bnorm, st, ctl);
+}
+
 __global__ void __launch_bounds__(KB) k_cg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
                                              const double* scal, const CgCtl* ctl) {
   if (ctl != nullptr && ctl->done) return;
@@ -1316,6 +1365,33 @@ int svb_cg_step_batched(svb_krylov* k, double bnorm, void* stream) {
   });
 }
 
+int svb_cg_step_batched_dia(svb_krylov* k, const svb_matrix* m, double bnorm, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k->ctl, SVB_INVALID, "svb_cg_batch_reset first");
+    SVB_REQUIRE(m && m->fmt == SVB_DIA && m->nrows == k->n && m->ncols == k->n, SVB_DIM_MISMATCH,
+                "fused CG step needs the square DIA operator of this workspace");
+    cudaStream_t s = S(stream);
+    double* P = ptr<double>(k->partials);
+    unsigned* C = ptr<unsigned>(k->counter);
+    CgCtl* ctl = ptr<CgCtl>(k->ctl);
+    double* sc = ptr<double>(k->scal);
+    if (!k->dparts) {
+      k->dgrid = grid_for(k->n, 256, 8);
+      k->dparts = alloc(k->dgrid * 8 + 64, s);
+      SVB_CUDA_TRY(cudaMemsetAsync(ptr<double>(k->dparts) + k->dgrid, 0, 64, s));
+    }
+    launch_dia_dot(m, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->p), ptr<double>(k->dparts),
+                   reinterpret_cast<unsigned*>(ptr<double>(k->dparts) + k->dgrid), sc + S_PQ, &ctl->done,
+                   k->dgrid, s);
+    k_cg_update_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
+                                            ptr<double>(k->q), sc, bnorm, P, C, k->st_dev, ctl);
+    SVB_CHECK_LAUNCH();
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), sc, ctl);
+    SVB_CHECK_LAUNCH();
+    mark(k, s);
+  });
+}
+
 int svb_cg_history(svb_krylov* k, int64_t first, int64_t count, double* host, void* stream) {
   return guard([&] {
     SVB_REQUIRE(k->hist && first >= 0 && first + count <= k->hist_cap, SVB_INVALID, "history range");
@@ -1334,6 +1410,7 @@ int svb_vecops_create(int64_t n, svb_vecops** out) {
     v->partials = alloc(v->grid * 8 + 64, 0);
     detach(v->partials);
     SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(v->partials->ptr) + v->grid * 8, 0, 64, 0));
+
     SVB_CUDA_TRY(cudaStreamSynchronize(0));
     *out = v;
   });

@@ -76,6 +76,10 @@ Buf upload(const void* host, size_t bytes, cudaStream_t s);
 Buf rows_to_ptr(const int32_t* rows, int64_t nnz, int64_t nrows, bool ptr64, cudaStream_t s);
 Buf ptr_to_rows(const svb_matrix* m, cudaStream_t s);
 void forget_bounds(const svb_matrix* m);  // drop cached LibC chunk bounds (spmv.cu)
+// DIA SpMV y = A x fused with sum dsrc.y into *out (spmv.cu, k_dia_dot);
+// partials holds >= max_grid doubles, counter is zero and left zero
+void launch_dia_dot(const svb_matrix* m, const double* x, double* y, const double* dsrc, double* partials,
+                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s);
 
 // exclusive scan of int64 counts (n+1 outputs; out[n] = total) and the total
 // copied back to the host (synchronises `s`)

@@ -733,6 +733,87 @@ __global__ void __launch_bounds__(256) k_dia(int64_t nrows, int64_t ncols, int64
   }
 }
 
+// DIA SpMV fused with the Krylov dot product that always follows it in CG
+// (q = A p, then p.q): the same per-row sums as k_dia (identical y), plus
+// sum_i dsrc[i] * y[i] folded per CTA and, in the last CTA to finish, over the
+// CTA partials in fixed order into *out (deterministic run to run).  The
+// separate p.q pass over 16n bytes disappears.  `skip` (batched CG's done
+// flag) turns the launch into a no-op after convergence.
+__global__ void __launch_bounds__(256) k_dia_dot(int64_t nrows, int64_t ncols, int64_t ndiag,
+                                                 const long long* __restrict__ offs, const double* __restrict__ data,
+                                                 const double* __restrict__ x, double* __restrict__ y,
+                                                 const double* __restrict__ dsrc, double* partials, unsigned* counter,
+                                                 double* out, const int* skip) {
+  if (skip != nullptr && *skip) return;
+  double dot = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    int64_t k = 0;
+    for (; k + 4 <= ndiag; k += 4) {
+      double v[4], xv[4];
+      bool in[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = i + __ldg(offs + k + u);
+        in[u] = j >= 0 && j < ncols;
+        v[u] = ld_stream(data + (k + u) * nrows + i);
+        xv[u] = in[u] ? ld_x(x + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (in[u]) acc = acc + v[u] * xv[u];
+    }
+    for (; k < ndiag; ++k) {
+      const int64_t j = i + __ldg(offs + k);
+      if (j >= 0 && j < ncols) acc = acc + ld_stream(data + k * nrows + i) * ld_x(x + j);
+    }
+    y[i] = acc;
+    dot = dot + dsrc[i] * acc;
+  }
+  __shared__ double sh[8];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) sh[wid] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < 8; ++w) b += sh[w];
+    partials[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;   // fixed-order fold of the CTA partials by the whole CTA
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(partials + b);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  if (lane == 0) sh[wid] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < 8; ++w) g += sh[w];
+    *out = g;
+    *counter = 0;
+  }
+}
+
+void launch_dia_dot(const svb_matrix* m, const double* x, double* y, const double* dsrc, double* partials,
+                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s) {
+  SVB_REQUIRE(m->fmt == SVB_DIA, SVB_UNSUPPORTED_CONFIG, "fused SpMV+dot needs a DIA matrix");
+  const int64_t n = m->nrows;
+  unsigned g = grid_for(n, 256, 8);   // the same grid as k_dia: full occupancy
+  SVB_REQUIRE(g <= max_grid, SVB_INVALID, "fused SpMV+dot: partials buffer too small");
+  k_dia_dot<<<g, 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), ptr<double>(m->vals), x, y, dsrc,
+                              partials, counter, out, skip);
+  SVB_CHECK_LAUNCH();
+}
+
 // spmv_reference (formats.py:419-435): strictly sequential row sums from 0.
 template <class P>
 __global__ void __launch_bounds__(256) k_csr_sequential(int64_t nrows, const P* __restrict__ ptr,

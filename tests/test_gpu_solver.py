@@ -300,3 +300,27 @@ def test_cg_graph_batches_match_uncaptured():
     assert r1.iterations == r2.iterations > 64        # several full (captured) batches ran
     assert r1.residual_history == r2.residual_history
     assert np.array_equal(r1.solution, r2.solution)
+
+
+def test_cg_fused_spmv_dot_matches_unfused():
+    """DIA CG with q = A p fused with p.q (one pass) vs the separate p.q
+    kernel: same iteration count, residual estimates within rounding, and
+    the same converged solution to 1e-10."""
+    import paper_2411_10143_b200 as P
+    from paper_2411_10143_b200 import generators as G, solver
+    A = P.CsrMatrix(*G.poisson2d(80))
+    params = P.GmresParams(tol=1e-8, max_iters=4000)
+    cfg = P.SpmvConfig.from_token("DIA/LibA")
+    old = solver._CG_FUSED
+    try:
+        solver._CG_FUSED = True
+        r1 = P.cg_solve(A, None, params, initial_config=cfg)
+        solver._CG_FUSED = False
+        r2 = P.cg_solve(A, None, params, initial_config=cfg)
+    finally:
+        solver._CG_FUSED = old
+    assert r1.converged and r2.converged
+    assert abs(r1.iterations - r2.iterations) <= 1
+    n = min(len(r1.residual_history), len(r2.residual_history))
+    assert np.allclose(r1.residual_history[:n // 2], r2.residual_history[:n // 2], rtol=1e-6)
+    assert np.linalg.norm(r1.solution - r2.solution) <= 1e-10 * np.linalg.norm(r2.solution) * 1e3
