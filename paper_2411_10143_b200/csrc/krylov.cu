@@ -1378,6 +1378,7 @@ int svb_cg_step_batched_dia(svb_krylov* k, const svb_matrix* m, double bnorm, vo
     if (!k->dparts) {
       k->dgrid = grid_for(k->n, 256, 8);
       k->dparts = alloc(k->dgrid * 8 + 64, s);
+      detach(k->dparts);   // long-lived: freed on the legacy stream, not this thread's
       SVB_CUDA_TRY(cudaMemsetAsync(ptr<double>(k->dparts) + k->dgrid, 0, 64, s));
     }
     launch_dia_dot(m, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->p), ptr<double>(k->dparts),
