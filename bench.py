@@ -316,14 +316,23 @@ def b200_arm(args):
     from paper_2411_10143_b200 import _lib, device
     from paper_2411_10143_b200.solver import DeviceOptions
 
+    # SPMVTUNE_DIST_BACKEND=gloo: every rank on the visible GPU(s) modulo their
+    # count, collectives staged through the host (HostStagedComm) — exercises
+    # the N > 1 path of this script on a one-GPU box; not a performance mode
+    host_staged = os.environ.get("SPMVTUNE_DIST_BACKEND") == "gloo"
+    if host_staged:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1 or args.workload == "config5":
         import torch.distributed as dist
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29517")
-            dist.init_process_group("nccl", rank=rank, world_size=ws,
-                                    device_id=torch.device("cuda", local))
+            if host_staged:
+                dist.init_process_group("gloo", rank=rank, world_size=ws)
+            else:
+                dist.init_process_group("nccl", rank=rank, world_size=ws,
+                                        device_id=torch.device("cuda", local))
         return dist_arm(args, ws, rank, local)
     L = _lib.lib()
 
@@ -525,7 +534,7 @@ def b200_arm(args):
         try:
             r = run_cpu_sample(1, 0, last.iterations)
             cpu = {"value": r["value"], "unit": "s", "cores": r["cores"], "kind": r["kind"],
-                   "sample": r["sample"], "phases": r["phases"]}
+                   "sample": r["sample"], "phases": r["phases"], "cpu_model": r.get("cpu_model")}
         except Exception as exc:  # measurement must not kill the bench line
             cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"[:300]}
@@ -580,8 +589,10 @@ def dist_arm(args, ws, rank, local):
 
     import paper_2411_10143_b200 as P
     from paper_2411_10143_b200 import _lib, device
-    from paper_2411_10143_b200.distributed import distributed_stencil_solve, stencil_block, \
-        stencil_partition
+    from paper_2411_10143_b200.distributed import HostStagedComm, distributed_stencil_solve, \
+        stencil_block, stencil_partition
+
+    comm_class = HostStagedComm if os.environ.get("SPMVTUNE_DIST_BACKEND") == "gloo" else None
 
     method, dims, offs, wts, workload = stencil_problem(args.workload)
     models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
@@ -595,6 +606,7 @@ def dist_arm(args, ws, rank, local):
     def step():
         t = {}
         res, _ = distributed_stencil_solve(method, dims, offs, wts, params, models=models, blk=blk,
+                                           comm_class=comm_class,
                                            timings=t)
         return res, t
 
@@ -618,7 +630,7 @@ def dist_arm(args, ws, rank, local):
     dist.barrier()
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
-    tt = torch.tensor([wall], device="cuda")
+    tt = torch.tensor([wall], device="cpu" if comm_class else "cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     value = float(tt.item()) / args.steps
 
@@ -658,6 +670,20 @@ def dist_arm(args, ws, rank, local):
     dist.all_gather_object(gathered, {"rank": rank, "rows": [int(bounds[rank]), int(bounds[rank + 1])],
                                       "spmv_ms": spmv_ms, "gbs": gbs, "gen_s": gen_s,
                                       "last_step": steps[-1]})
+    cpu = None
+    if rank == 0 and ws == 1 and args.workload == "config5" and not args.no_cpu:
+        try:
+            env = dict(os.environ)
+            env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+            env.pop("CUDA_VISIBLE_DEVICES", None)
+            cmd = [sys.executable, "-m", "oracle.bench_cpu", "--laplace27", "120", "--iters", "4",
+                   "--total-iters", str(results[-1]["iterations"]), "--target", str(dims[0])]
+            o = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+            r = json.loads(o.stdout.strip().splitlines()[-1])
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+        except Exception as exc:  # measurement must not kill the bench line
+            cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"[:300]}
     if rank == 0:
         line = {"metric": "CG/GMRES time-to-solution incl. preprocessing (global features+cascade+"
                           "conversion), row-partitioned",
@@ -666,7 +692,7 @@ def dist_arm(args, ws, rank, local):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload, "parallelism": f"row-partitioned x{ws}",
                            "l2": "inputs larger than L2"},
-                "roofline": roofline, "cpu_baseline": None,
+                "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": None, "gpu_launches": int(launches), "clocks": clk,
                 "detail": {"results": results[-1], "per_step": steps, "per_rank": gathered,
                            "per_iteration_solve_s": per_iter,

@@ -49,6 +49,58 @@ def convdiff9_csr(nx: int, diag: float = 8.5, beta: float = 0.25) -> O.OCsr:
     return O.OCsr(n, n, ptr, c2.T[masks.T], np.ascontiguousarray(v2.T[masks.T]))
 
 
+def laplace27_csr(n3: int) -> O.OCsr:
+    """3-D 27-point Laplacian n3^3 (diag 26, off -1), same structure as
+    paper_2411_10143_b200.generators.laplace27 (restated: the oracle never
+    imports the product)."""
+    n = n3 ** 3
+    z, rem = np.divmod(np.arange(n, dtype=np.int64), n3 * n3)
+    y, x = np.divmod(rem, n3)
+    cols, vals, masks = [], [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                masks.append((x + dx >= 0) & (x + dx < n3) & (y + dy >= 0) & (y + dy < n3) &
+                             (z + dz >= 0) & (z + dz < n3))
+                cols.append(np.arange(n, dtype=np.int64) + (dz * n3 + dy) * n3 + dx)
+                vals.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+    masks = np.stack(masks)
+    ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(masks.sum(axis=0), out=ptr[1:])
+    c2 = np.stack(cols)
+    v2 = np.broadcast_to(np.asarray(vals)[:, None], masks.shape)
+    return O.OCsr(n, n, ptr, c2.T[masks.T], np.ascontiguousarray(v2.T[masks.T]))
+
+
+def cg_sample(n3: int, iters: int, total_iters: int, target_n3: int, models) -> dict:
+    """Config 5 on the CPU: the reference's predict-then-solve with the new CG
+    oracle on a n3^3 grid, `iters` CG iterations timed; preprocessing and the
+    per-iteration time are scaled per nnz to target_n3^3 and the solve to
+    total_iters iterations (the full 600^3 matrix does not fit the host)."""
+    csr = laplace27_csr(n3)
+    b = O.spmv_sequential(csr, np.ones(csr.nrows))
+    t = {}
+    t0 = time.perf_counter()
+    coo = O.csr_to_coo(csr)
+    fv = O.features(O.coo_to_csr(coo))
+    t["features"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    final = O.cascade(models, fv)[-1]
+    t["inference"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rep = O.convert(coo, final.split("/")[0])
+    t["conversion"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = O.cg(lambda v: O.spmv(final, rep, v, workers=4), b, tol=1e-300, max_iters=iters)
+    per_it = (time.perf_counter() - t0) / max(1, res["iterations"])
+    nnz, tnnz = csr.cols.size, (3 * target_n3 - 2) ** 3
+    scale = tnnz / nnz
+    prep = (t["features"] + t["inference"] + t["conversion"]) * scale
+    value = prep + per_it * scale * total_iters
+    return {"value": value, "phases": {k: v * scale for k, v in t.items()}, "config": final,
+            "per_iteration_s": per_it * scale, "sampled_nnz": int(nnz), "target_nnz": int(tnnz)}
+
+
 def load_models():
     d = ROOT / "tests" / "golden" / "models"
     return {p.stem: json.loads(p.read_text()) for p in d.glob("*.json")}
@@ -90,6 +142,16 @@ def sample(csr: O.OCsr, models, iters: int, total_iters: int, b: np.ndarray) -> 
             "sampled_iterations": res["iterations"], "fit": [float(icpt), float(slope)]}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--nx", type=int, default=2000)
@@ -97,7 +159,23 @@ def main(argv=None):
     ap.add_argument("--total-iters", type=int, default=77)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=0)
+    ap.add_argument("--laplace27", type=int, default=0,
+                    help="config 5 mode: sample grid size (the solve is extrapolated per nnz)")
+    ap.add_argument("--target", type=int, default=600, help="config 5: grid size extrapolated to")
     a = ap.parse_args(argv)
+    if a.laplace27:
+        r = cg_sample(a.laplace27, a.iters, a.total_iters, a.target, load_models())
+        print(json.dumps({"value": r["value"], "unit": "s", "cores": os.cpu_count(),
+                          "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS"), "kind": "port",
+                          "cpu_model": cpu_model(),
+                          "sample": (f"reference predict-then-solve with the CG oracle on the 27-point "
+                                     f"Laplacian {a.laplace27}^3 (nnz={r['sampled_nnz']:,}), "
+                                     f"{a.iters} CG iterations timed; preprocessing and per-iteration "
+                                     f"time scaled per nnz to {a.target}^3 (nnz={r['target_nnz']:,}) and "
+                                     f"the solve to {a.total_iters} iterations (EXTRAPOLATED)"),
+                          "phases": r["phases"], "config": r["config"],
+                          "per_iteration_s": r["per_iteration_s"]}))
+        return 0
     t_gen = time.perf_counter()
     csr = convdiff9_csr(a.nx)
     b = O.spmv_sequential(csr, np.ones(csr.nrows))        # RHS outside the clock (solver.py:355)
@@ -110,7 +188,7 @@ def main(argv=None):
     out = {"value": vals[len(vals) // 2], "values": [r["value"] for r in runs],
            "unit": "s", "cores": os.cpu_count(),
            "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
-           "kind": "port",
+           "kind": "port", "cpu_model": cpu_model(),
            "sample": (f"reference predict-then-solve on conv-diff9 {a.nx}^2 "
                       f"(n={csr.nrows}, nnz={csr.cols.size}): features+cascade+conversion "
                       f"in full, {runs[0]['sampled_iterations']} GMRES(30) iterations timed "
