@@ -308,6 +308,12 @@ def config1_cg(P, device, _lib, models, start_cfg, reps: int = 3) -> dict:
 # ---------------------------------------------------------------------------
 def b200_arm(args):
     ws, rank, local = dist_env()
+    # SPMVTUNE_DIST_BACKEND=gloo: every rank on GPU 0, collectives staged
+    # through the host (HostStagedComm) — exercises the N > 1 path of this
+    # script on a one-GPU box; not a performance mode
+    host_staged = os.environ.get("SPMVTUNE_DIST_BACKEND") == "gloo"
+    if host_staged:
+        local = 0
     os.environ.setdefault("SPMVTUNE_DEVICE", str(local))
     import numpy as np
     import torch
@@ -316,12 +322,6 @@ def b200_arm(args):
     from paper_2411_10143_b200 import _lib, device
     from paper_2411_10143_b200.solver import DeviceOptions
 
-    # SPMVTUNE_DIST_BACKEND=gloo: every rank on the visible GPU(s) modulo their
-    # count, collectives staged through the host (HostStagedComm) — exercises
-    # the N > 1 path of this script on a one-GPU box; not a performance mode
-    host_staged = os.environ.get("SPMVTUNE_DIST_BACKEND") == "gloo"
-    if host_staged:
-        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1 or args.workload == "config5":
         import torch.distributed as dist
@@ -691,6 +691,8 @@ def dist_arm(args, ws, rank, local):
                 "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload, "parallelism": f"row-partitioned x{ws}",
+                           "comm": "gloo, host-staged (path validation, not a performance number)"
+                           if comm_class else "nccl",
                            "l2": "inputs larger than L2"},
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": None, "gpu_launches": int(launches), "clocks": clk,
