@@ -282,6 +282,8 @@ __global__ void __launch_bounds__(TILE_ROWS) k_diag_bits(int64_t nrows, const in
                                                          const int* __restrict__ cols, unsigned* __restrict__ bits) {
   constexpr int CAP = 8192;
   __shared__ int scol[CAP];
+  __shared__ long long dcache[DIAG_CACHE];
+  diag_cache_init(dcache);
   const int64_t ntiles = (nrows + TILE_ROWS - 1) / TILE_ROWS;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const StagedRows<int64_t> t = stage_row_tile<int64_t, TILE_ROWS, CAP>(tile, nrows, ptr, cols, scol);
@@ -289,10 +291,7 @@ __global__ void __launch_bounds__(TILE_ROWS) k_diag_bits(int64_t nrows, const in
     if (i >= t.r1) continue;
     for (int64_t k = ptr[i] - t.base, e = ptr[i + 1] - t.base; k < e; ++k) {
       const int c = t.staged ? scol[k] : __ldg(cols + t.base + k);
-      const int64_t d = (int64_t)c - i + nrows - 1;
-      const unsigned m = 1u << (d & 31);
-      unsigned* w = bits + (d >> 5);
-      if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+      mark_diag(bits, (long long)c - i + nrows - 1, dcache);
     }
   }
 }

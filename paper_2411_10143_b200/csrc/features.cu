@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __re
                                                     unsigned* __restrict__ bits, FeatAcc* out) {
   constexpr int CAP = 8192;  // staged column indices per tile (32 KB)
   __shared__ int scol[CAP];
+  __shared__ long long dcache[DIAG_CACHE];
+  diag_cache_init(dcache);   // (the tile loop's first __syncthreads orders it)
   FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
   const int64_t ntiles = (nrows + BLOCK - 1) / BLOCK;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -75,10 +77,7 @@ __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __re
     int prev = c0;
     int64_t run = 1, best = 1;
     for (int64_t k = s;;) {
-      const int64_t d = (int64_t)prev + diag0;
-      const unsigned m = 1u << (d & 31);
-      unsigned* w = bits + (d >> 5);
-      if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+      mark_diag(bits, (long long)prev + diag0, dcache);
       if (++k >= e) break;
       const int c = col(k);
       run = (c == prev + 1) ? run + 1 : 1;

@@ -121,4 +121,21 @@ __device__ __forceinline__ StagedRows<P> stage_row_tile(int64_t tile, int64_t nr
   return t;
 }
 
+// Diagonal-occupancy bitmap marking with a per-CTA direct-mapped cache of
+// diagonal indices already set: a stencil or banded matrix touches a handful
+// of diagonals, so nearly every entry hits the cache and the global bitmap
+// sees one read/atomicOr per (CTA, diagonal) instead of one per entry.
+constexpr int DIAG_CACHE = 512;
+__device__ __forceinline__ void diag_cache_init(long long* cache) {
+  for (int k = threadIdx.x; k < DIAG_CACHE; k += blockDim.x) cache[k] = -1;
+}
+__device__ __forceinline__ void mark_diag(unsigned* __restrict__ bits, long long d, long long* cache) {
+  const int slot = (int)(d & (DIAG_CACHE - 1));
+  if (*(volatile long long*)(cache + slot) == d) return;
+  const unsigned m = 1u << (d & 31);
+  unsigned* w = bits + (d >> 5);
+  if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+  cache[slot] = d;   // racy but benign: a stale slot only costs a global check
+}
+
 }  // namespace svb
