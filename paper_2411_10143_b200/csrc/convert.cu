@@ -437,12 +437,12 @@ static svb_matrix* build_dia(const RowView& v, cudaStream_t s) {
                                                             ptr<int64_t>(pos), ptr<long long>(m->offs));
     SVB_CHECK_LAUNCH();
     const size_t dsm = (size_t)DIA_TILE_CAP * 12 + (size_t)ndiag * 8;
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {   // once per process (thread-safe static init)
       SVB_CUDA_TRY(cudaFuncSetAttribute(k_csr_to_dia, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)((size_t)DIA_TILE_CAP * 12 + (size_t)DIA_CAP * 8)));
-      attr = true;
-    }
+      return true;
+    }();
+    (void)attr;
     k_csr_to_dia<<<grid_for(v.nrows, TILE_ROWS, 4), TILE_ROWS, dsm, s>>>(v.nrows, ndiag, ptr<long long>(m->offs),
                                                                    ptr<int64_t>(v.ptr), ptr<int>(v.cols),
                                                                    ptr<double>(v.vals), ptr<double>(m->vals));

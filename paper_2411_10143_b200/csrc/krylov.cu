@@ -702,21 +702,21 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_tmem(Gm G, int j, double bnorm
   }
 }
 
-// back-substitution of the rotated system (solver.py:211-214), one thread
-__global__ void k_gm_solve_y(Gm G, int j) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int m = G.m;
-  for (int i = j; i >= 0; --i) {
-    double dot = 0.0;
-    for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * G.y[k];
-    G.y[i] = (G.g[i] - dot) / G.H[i * m + i];
-  }
-}
-
-// x += V[:j+1]^T y (solver.py:215-216, 339-340)
+// x += V[:j+1]^T y (solver.py:215-216, 339-340).  Every CTA first solves the
+// (j+1)x(j+1) triangular system for y itself (solver.py:211-214, at most
+// ~1K flops, from H in L2), which replaces a separate one-thread launch.
 __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restrict__ x) {
   __shared__ double ys[64];
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) ys[i] = G.y[i];
+  if (threadIdx.x == 0) {
+    const int m = G.m;
+    for (int i = j; i >= 0; --i) {
+      double dot = 0.0;
+      for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * ys[k];
+      ys[i] = (G.g[i] - dot) / G.H[i * m + i];
+    }
+    if (blockIdx.x == 0)
+      for (int i = 0; i <= j; ++i) G.y[i] = ys[i];
+  }
   __syncthreads();
   for_pairs(
       G.n,
@@ -1284,9 +1284,7 @@ int svb_gmres_normalize(svb_krylov* k, int32_t j, void* stream) {
 int svb_gmres_update_x(svb_krylov* k, int32_t j, void* stream) {
   return guard([&] {
     Gm G = gm_of(k);
-    k_gm_solve_y<<<1, 32, 0, S(stream)>>>(G, j);
     k_gm_update_x<<<k->rgrid, KB, 0, S(stream)>>>(G, j, ptr<double>(k->x));
-    note_launches(1);
     SVB_CHECK_LAUNCH();
   });
 }
