@@ -49,6 +49,7 @@ NX = 2000
 TOL = 1e-8
 RESTART = 30
 METRIC = "GMRES(30) time-to-solution incl. preprocessing (features+cascade+conversion)"
+METRIC5 = "CG time-to-solution incl. preprocessing (features+cascade+conversion)"
 WORKLOAD = (f"config2: GMRES({RESTART}) fp64, tol {TOL:g}, b=A*1, nonsymmetric 9-point "
             f"convection-diffusion {NX}x{NX} (n={NX * NX:,}, nnz={(3 * NX - 2) ** 2:,}); async "
             "predict-while-solve starting on CSR/LibA/32 with the reference's shipped cascade "
@@ -90,17 +91,34 @@ def reference_arm(args):
     if rank != 0:
         return
     t0 = time.perf_counter()
-    r = run_cpu_sample(args.steps, args.warmup, args.total_iters)
-    line = {"metric": METRIC, "value": r["value"], "unit": "s", "n_gpus": args.gpus,
+    if args.workload == "config5":
+        # the 600^3 matrix does not fit the host: a 120^3 sample, extrapolated
+        env = dict(os.environ)
+        env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+        env.pop("CUDA_VISIBLE_DEVICES", None)
+        vals = []
+        for _ in range(args.warmup + args.steps):
+            o = subprocess.run([sys.executable, "-m", "oracle.bench_cpu", "--laplace27", "120", "--iters", "4",
+                                "--total-iters", "763", "--target", "600"], cwd=ROOT, env=env,
+                               capture_output=True, text=True, timeout=1800)
+            vals.append(json.loads(o.stdout.strip().splitlines()[-1]))
+        r = vals[-1]
+        r["values"] = [v["value"] for v in vals[args.warmup:]]
+        r["value"] = statistics.median(r["values"])
+        metric, workload = METRIC5, stencil_problem("config5")[4]
+    else:
+        r = run_cpu_sample(args.steps, args.warmup, args.total_iters)
+        metric, workload = METRIC, WORKLOAD
+    line = {"metric": metric, "value": r["value"], "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"] * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "mode": "sequential predict-then-solve (CPU)"},
+            "config": {"workload": workload, "mode": "sequential predict-then-solve (CPU)"},
             "cpu_baseline": {"value": r["value"], "unit": "s", "cores": r["cores"],
                              "kind": r["kind"], "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "detail": {"phases": r["phases"], "values": r["values"], "config": r["config"],
+            "detail": {"phases": r["phases"], "values": r.get("values"), "config": r["config"],
                        "wall_seconds": time.perf_counter() - t0}}
     print(json.dumps(line), flush=True)
 
@@ -685,8 +703,7 @@ def dist_arm(args, ws, rank, local):
             cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"[:300]}
     if rank == 0:
-        line = {"metric": "CG/GMRES time-to-solution incl. preprocessing (global features+cascade+"
-                          "conversion), row-partitioned",
+        line = {"metric": METRIC5 if args.workload == "config5" else METRIC,
                 "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
