@@ -173,7 +173,7 @@ class NvmlClockSampler:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index: int, period: float = 0.25):
+    def __init__(self, index: int, period: float = 0.02):
         import pynvml
         self.nv = pynvml
         pynvml.nvmlInit()
