@@ -41,6 +41,11 @@ struct svb_matrix {
   // COO: row-run starts (int64 row pointer derived from the sorted rows —
   // what np.flatnonzero(np.diff(rows)) computes on every reference call)
   mutable svb::Buf dptr;
+  // HYB: the spill rows that have entries, compacted (run pointer int64
+  // [nhruns+1] into the spill arrays, row of each run int32 [nhruns]), so
+  // the spill kernel never tiles the rows that spill nothing
+  mutable int64_t nhruns = -1;
+  mutable svb::Buf hruns, hmap;
 
   int64_t device_bytes() const {
     int64_t b = 0;

@@ -466,7 +466,8 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
                                                            int nb, int lanes, int64_t nlong,
                                                            const int* __restrict__ lrow,
                                                            const int64_t* __restrict__ lbeg,
-                                                           const int64_t* __restrict__ lend) {
+                                                           const int64_t* __restrict__ lend,
+                                                           const int* __restrict__ rowmap) {
   using L = PipeLayout<T, P, CAP, NS>;
   constexpr int U = CAP / ROWSEG_ROWS;  // products per thread per tile (one round of gathers)
   static_assert(CAP % ROWSEG_ROWS == 0 && CAP >= MED_ROW, "tile capacity");
@@ -559,7 +560,8 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
     } else {
       if (thread_row) v = pw_row_value<T>(get_s, s, e, bounds, nb);
     }
-    const int64_t row = (int64_t)t.r0 + tid;
+    // tile rows are matrix rows, or (HYB spill) compacted runs mapped to rows
+    const int64_t row = rowmap ? (int64_t)(mine ? rowmap[t.r0 + tid] : 0) : (int64_t)t.r0 + tid;
     if (thread_row) {
       if (!ADD) y[row] = v;
       else if (len > 0) y[row] = y[row] + v;   // HYB spill: rows with entries only
@@ -572,8 +574,9 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
       if constexpr (LANE) w = warp_lane_row<T>(get_s, s2, e2 - s2, lanes);
       else w = warp_pw_row<MED_LEAVES, T>(get_s, s2, e2, bounds, nb, loff[warp], llen[warp], lsum[warp]);
       if (lane == 0) {
-        if (!ADD) y[(int64_t)t.r0 + rr] = w;
-        else y[(int64_t)t.r0 + rr] = y[(int64_t)t.r0 + rr] + w;
+        const int64_t yr = rowmap ? (int64_t)rowmap[t.r0 + rr] : (int64_t)t.r0 + rr;
+        if (!ADD) y[yr] = w;
+        else y[yr] = y[yr] + w;
       }
     }
     __syncthreads();  // stage st and the medium-row list are free again
@@ -904,16 +907,53 @@ static const long long* coo_runs(const svb_matrix* m, cudaStream_t s) {
 // rows of a row pointer longer than MED_ROW -> (row, begin, end) list
 template <class P>
 __global__ void k_find_long(int64_t nrows, const P* __restrict__ ptr, unsigned long long* count, int* lrow,
-                            int64_t* lbeg, int64_t* lend) {
+                            int64_t* lbeg, int64_t* lend, const int* __restrict__ rowmap = nullptr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = ptr[i], e = ptr[i + 1];
     if (e - b > MED_ROW) {
       const unsigned long long k = atomicAdd(count, 1ull);
-      lrow[k] = (int)i;
+      lrow[k] = rowmap ? rowmap[i] : (int)i;
       lbeg[k] = b;
       lend[k] = e;
     }
   }
+}
+
+__global__ void k_spill_flags(int64_t n, const long long* __restrict__ ptr, int64_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    f[i] = ptr[i + 1] > ptr[i] ? 1 : 0;
+}
+__global__ void k_spill_compact(int64_t n, const long long* __restrict__ ptr, const int64_t* __restrict__ pos,
+                                long long* __restrict__ runs, int* __restrict__ map, int64_t nruns) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (ptr[i + 1] > ptr[i]) {
+      runs[pos[i]] = ptr[i];
+      map[pos[i]] = (int)i;
+    }
+    if (i == n - 1) runs[nruns] = ptr[n];
+  }
+}
+
+// HYB spill rows with entries, compacted (built once, cached on the handle)
+static int64_t hyb_runs(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->nhruns >= 0) return m->nhruns;
+  const int64_t n = m->nrows;
+  Buf f = alloc((n + 1) * 8, s), pos = alloc((n + 1) * 8, s);
+  const unsigned g = grid_for(n, 256);
+  k_spill_flags<<<g, 256, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int64_t>(f));
+  SVB_CHECK_LAUNCH();
+  const int64_t nr = exclusive_scan_total(ptr<int64_t>(f), ptr<int64_t>(pos), n, s);
+  m->hruns = alloc((nr + 1) * 8, s);
+  m->hmap = alloc((nr > 0 ? nr : 1) * 4, s);
+  k_spill_compact<<<g, 256, 0, s>>>(n, ptr<long long>(m->ptr), ptr<int64_t>(pos), ptr<long long>(m->hruns),
+                                    ptr<int>(m->hmap), nr);
+  SVB_CHECK_LAUNCH();
+  SVB_CUDA_TRY(cudaStreamSynchronize(s));
+  detach(m->hruns);
+  detach(m->hmap);
+  m->nhruns = nr;
+  return nr;
 }
 
 // The handle's long-segment list (built once, cached): CSR rows, COO runs
@@ -942,8 +982,11 @@ static int64_t long_list(const svb_matrix* m, cudaStream_t s) {
     else run(ptr<int>(m->ptr));
   } else if (m->fmt == SVB_COO) {
     run(ptr<long long>(m->dptr));
-  } else {  // HYB: spill row pointer (int64)
-    run(ptr<long long>(m->ptr));
+  } else {  // HYB: the compacted spill runs, rows through the run map
+    k_find_long<<<grid_for(m->nhruns > 0 ? m->nhruns : 1, 256), 256, 0, s>>>(
+        m->nhruns, ptr<long long>(m->hruns), ptr<unsigned long long>(cnt), ptr<int>(m->lrow),
+        ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend), ptr<int>(m->hmap));
+    SVB_CHECK_LAUNCH();
   }
   unsigned long long h = 0;
   SVB_CUDA_TRY(cudaMemcpyAsync(&h, cnt->ptr, 8, cudaMemcpyDeviceToHost, s));
@@ -958,15 +1001,16 @@ template <class P>
 static int64_t tile_list(const svb_matrix* m, const P* rp, int cap, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(m->mu);
   if (m->ntiles >= 0 && m->tile_cap == cap) return m->ntiles;
-  const int64_t nblk = (m->nrows + ROWSEG_ROWS - 1) / ROWSEG_ROWS;
+  const int64_t nrows = m->fmt == SVB_HYB ? m->nhruns : m->nrows;   // HYB: compacted spill runs
+  const int64_t nblk = (nrows + ROWSEG_ROWS - 1) / ROWSEG_ROWS;
   Buf cnt = alloc((nblk + 1) * 8, s), off = alloc((nblk + 1) * 8, s);
   const unsigned g = grid_for(nblk, 128);
-  k_make_tiles<P><<<g, 128, 0, s>>>(m->nrows, rp, cap, ptr<int64_t>(cnt), nullptr, nullptr);
+  k_make_tiles<P><<<g, 128, 0, s>>>(nrows, rp, cap, ptr<int64_t>(cnt), nullptr, nullptr);
   SVB_CHECK_LAUNCH();
   const int64_t total = exclusive_scan_total(ptr<int64_t>(cnt), ptr<int64_t>(off), nblk, s);
   Buf tiles = alloc((total > 0 ? total : 1) * sizeof(RowTile), s);
   if (total > 0) {
-    k_make_tiles<P><<<g, 128, 0, s>>>(m->nrows, rp, cap, nullptr, ptr<int64_t>(off), ptr<RowTile>(tiles));
+    k_make_tiles<P><<<g, 128, 0, s>>>(nrows, rp, cap, nullptr, ptr<int64_t>(off), ptr<RowTile>(tiles));
     SVB_CHECK_LAUNCH();
   }
   SVB_CUDA_TRY(cudaStreamSynchronize(s));  // an older tile list may still be in use elsewhere
@@ -997,7 +1041,7 @@ static void launch_rows_cfg(const svb_matrix* m, const P* rp, const int* cols, c
   const unsigned g = (unsigned)(work < cap ? work : cap);
   k_rows_pipe<T, P, ADD, LANE, CAP, NS><<<g, ROWSEG_ROWS, L::BYTES, s>>>(
       nt, ptr<RowTile>(m->tiles), rp, cols, vals, x, y, bounds, nb, lanes, nl, ptr<int>(m->lrow),
-      ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend));
+      ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend), m->fmt == SVB_HYB ? ptr<int>(m->hmap) : nullptr);
   SVB_CHECK_LAUNCH();
 }
 
@@ -1012,7 +1056,8 @@ static void launch_rows(const svb_matrix* m, const P* rp, const int* cols, const
     return e ? atoi(e) : 0;
   }();
   const int64_t entries = m->fmt == SVB_HYB ? m->spill_nnz : m->nnz;
-  const double per_block = m->nrows ? (double)entries * ROWSEG_ROWS / (double)m->nrows : 0.0;
+  const int64_t trows = m->fmt == SVB_HYB ? m->nhruns : m->nrows;   // HYB: compacted spill runs
+  const double per_block = trows > 0 ? (double)entries * ROWSEG_ROWS / (double)trows : 0.0;
   const int cfg = forced ? forced : per_block <= 900 ? 3 : per_block <= 1400 ? 1 : 2;
   auto go = [&](auto lane_tag) {
     constexpr bool LANE = decltype(lane_tag)::value;
@@ -1079,8 +1124,11 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
   } else {  // HYB
     k_ell_sweep<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), vals, x, y);
     SVB_CHECK_LAUNCH();
-    if (m->spill_nnz > 0)
-      launch_rows<T, long long, true>(m, ptr<long long>(m->ptr), ptr<int>(m->scols), svals, x, y, nullptr, 0, 0, s);
+    if (m->spill_nnz > 0) {
+      hyb_runs(m, s);
+      launch_rows<T, long long, true>(m, ptr<long long>(m->hruns), ptr<int>(m->scols), svals, x, y, nullptr, 0, 0,
+                                      s);
+    }
     return;
   }
   SVB_CHECK_LAUNCH();
