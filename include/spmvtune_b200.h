@@ -128,6 +128,11 @@ int svb_coo_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
 int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr_host,
                    const int64_t* col_idx_host, const double* vals_host, void* stream,
                    svb_matrix** out);
+/* Rows [r0, r1) of a CSR matrix as a new CSR (same ncols, rebased row
+ * pointer): the interior / boundary row blocks of a row-partitioned rank,
+ * whose interior SpMV overlaps the halo exchange. */
+int svb_csr_row_slice(const svb_matrix* src, int64_t r0, int64_t r1, void* stream,
+                      svb_matrix** out);
 /* EllMatrix(nrows, ncols, width, col_idx, values): column-major (nrows x width)
  * arrays, i.e. cell (i, k) at k*nrows + i; sentinel column = ncols. */
 int svb_ell_create(int64_t nrows, int64_t ncols, int64_t width, const int64_t* cols_host,

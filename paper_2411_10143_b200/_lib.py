@@ -90,6 +90,7 @@ _SIGS = {
     "svb_graph_end": [_P, _PP],
     "svb_graph_launch": [_P, _P],
     "svb_graph_destroy": [_P],
+    "svb_csr_row_slice": [_P, C.c_int64, C.c_int64, _P, _PP],
     "svb_csr_stencil_rows": [C.c_int, _PI64, C.c_int, C.POINTER(C.c_int32), _PD, C.c_int64, C.c_int64,
                              C.c_int64, C.c_int64, _P, _PP],
     "svb_convert": [_P, C.c_int, _I64, _P, _PP],

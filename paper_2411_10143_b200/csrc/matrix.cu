@@ -80,6 +80,15 @@ __global__ void k_to_f32(const double* __restrict__ src, float* __restrict__ dst
     dst[i] = (float)src[i];
 }
 
+// rows [r0, r0 + n) of a row pointer, rebased to start at 0
+template <class Pin, class Pout>
+__global__ void k_rebase_ptr(const Pin* __restrict__ src, Pout* __restrict__ dst, int64_t n1) {
+  const int64_t base = (int64_t)src[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (Pout)((int64_t)src[i] - base);
+}
+
 void narrow_i64_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   k_narrow<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
@@ -409,6 +418,52 @@ int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
     else m->ptr = upload_i32(row_ptr_host, nrows + 1, s);
     m->cols = upload_i32(col_idx_host, nnz, s);
     m->vals = upload(vals_host, nnz * 8, s);
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = publish(m);
+  });
+}
+
+int svb_csr_row_slice(const svb_matrix* src, int64_t r0, int64_t r1, void* stream,
+                      svb_matrix** out) {
+  return guard([&] {
+    SVB_REQUIRE(src && src->fmt == SVB_CSR, SVB_UNSUPPORTED_CONFIG, "row slice needs a CSR matrix");
+    SVB_REQUIRE(0 <= r0 && r0 < r1 && r1 <= src->nrows, SVB_DIM_MISMATCH,
+                "row slice must be a non-empty range inside the matrix");
+    cudaStream_t s = S(stream);
+    int64_t b[2];
+    if (src->ptr64) {
+      SVB_CUDA_TRY(cudaMemcpyAsync(&b[0], ptr<int64_t>(src->ptr) + r0, 8, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaMemcpyAsync(&b[1], ptr<int64_t>(src->ptr) + r1, 8, cudaMemcpyDeviceToHost, s));
+    } else {
+      int32_t b32[2];
+      SVB_CUDA_TRY(cudaMemcpyAsync(&b32[0], ptr<int32_t>(src->ptr) + r0, 4, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaMemcpyAsync(&b32[1], ptr<int32_t>(src->ptr) + r1, 4, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+      b[0] = b32[0]; b[1] = b32[1];
+    }
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    auto m = new svb_matrix();
+    m->fmt = SVB_CSR;
+    m->nrows = r1 - r0; m->ncols = src->ncols; m->nnz = b[1] - b[0];
+    m->ptr64 = m->nnz >= INT32_MAX;
+    const int64_t n1 = m->nrows + 1;
+    m->ptr = alloc(n1 * (m->ptr64 ? 8 : 4), s);
+    const int g = grid_for(n1, 256);
+    if (src->ptr64 && m->ptr64)
+      k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int64_t>(src->ptr) + r0, ptr<int64_t>(m->ptr), n1);
+    else if (src->ptr64)
+      k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int64_t>(src->ptr) + r0, ptr<int32_t>(m->ptr), n1);
+    else
+      k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int32_t>(src->ptr) + r0, ptr<int32_t>(m->ptr), n1);
+    SVB_CHECK_LAUNCH();
+    m->cols = alloc(m->nnz * 4, s);
+    m->vals = alloc(m->nnz * 8, s);
+    if (m->nnz) {
+      SVB_CUDA_TRY(cudaMemcpyAsync(m->cols->ptr, ptr<int32_t>(src->cols) + b[0], m->nnz * 4,
+                                   cudaMemcpyDeviceToDevice, s));
+      SVB_CUDA_TRY(cudaMemcpyAsync(m->vals->ptr, ptr<double>(src->vals) + b[0], m->nnz * 8,
+                                   cudaMemcpyDeviceToDevice, s));
+    }
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
     *out = publish(m);
   });

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -38,7 +39,7 @@ from .formats import CsrMatrix, FormatTag, convert
 from .kernels import Library, SpmvConfig, default_workers, launch
 
 __all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
-           "NcclComm", "HostStagedComm", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
+           "NcclComm", "HostStagedComm", "interior_rows", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
            "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve"]
 
 
@@ -190,6 +191,39 @@ class HaloPlan:
         return 8 * sum(hi - lo for _, lo, hi in self.recvs)
 
 
+def interior_rows(block: LocalBlock, min_fraction: float = 0.25):
+    """(ia, ib): the longest contiguous run of local rows whose columns all
+    lie in this rank's own rows, so their SpMV can run while the halo
+    exchange is in flight; None when there is no halo or the run is below
+    ``min_fraction`` of the rows (irregular matrices: nearly every row reads
+    a remote column)."""
+    n, own = block.nloc, block.r0 - block.cmin
+    if n == 0 or (block.cmin >= block.r0 and block.cmax <= block.r1 - 1):
+        return None
+    if block.row_ptr is None:
+        # device-generated stencil slab: row i reads [i + lo, i + hi] (global
+        # diagonal offsets), clipped to the grid
+        lo, hi = (int(block.offsets.min()), int(block.offsets.max())) if block.offsets.size else (0, 0)
+        ia = min(n, max(0, -lo)) if block.cmin < block.r0 else 0
+        ib = max(ia, n - max(0, hi)) if block.cmax > block.r1 - 1 else n
+    else:
+        ptr = np.asarray(block.row_ptr, dtype=np.int64)
+        lens = np.diff(ptr)
+        flagged = np.zeros(n, dtype=bool)
+        nz = np.flatnonzero(lens)
+        if nz.size:
+            starts = ptr[nz]
+            cmin = np.minimum.reduceat(block.cols, starts)
+            cmax = np.maximum.reduceat(block.cols, starts)
+            flagged[nz] = (cmin < own) | (cmax >= own + n)
+        pos = np.concatenate(([-1], np.flatnonzero(flagged), [n]))
+        k = int(np.argmax(np.diff(pos)))
+        ia, ib = int(pos[k]) + 1, int(pos[k + 1])
+    if ib - ia < max(1, int(min_fraction * n)):
+        return None
+    return ia, ib
+
+
 # ---------------------------------------------------------------------------
 # device implementations of the two interfaces
 # ---------------------------------------------------------------------------
@@ -307,6 +341,18 @@ class CudaOps:
         csr = self.local_csr(block)
         return csr if cfg.format is FormatTag.CSR else convert(csr, cfg.format)
 
+    def prepare_rows(self, block: LocalBlock, cfg: SpmvConfig, a: int, b: int):
+        """Rows [a, b) of the local block in cfg's format (svb_csr_row_slice
+        of the local CSR, cached, then converted)."""
+        cache = block.__dict__.setdefault("_row_slices", {})
+        csr = cache.get((a, b))
+        if csr is None:
+            from .formats import _new_handle
+            dev = _new_handle(self.L.svb_csr_row_slice, self.local_csr(block)._device().handle,
+                              int(a), int(b), self.stream.handle)
+            csr = cache[(a, b)] = CsrMatrix._wrap(dev)
+        return csr if cfg.format is FormatTag.CSR else convert(csr, cfg.format)
+
 
 class NcclComm:
     """torch.distributed (NCCL) collectives ordered on the solver stream."""
@@ -337,12 +383,23 @@ class NcclComm:
         return out
 
     def exchange(self, sends, recvs):
+        self.exchange_finish(self.exchange_start(sends, recvs))
+
+    def exchange_start(self, sends, recvs):
+        """Enqueue the halo sends/receives behind the work already on the
+        solver stream (NCCL's stream waits for it) without making the solver
+        stream wait for them: kernels enqueued next overlap the transfer."""
         ops = [self.dist.P2POp(self.dist.isend, self._t(v), peer) for peer, v in sends]
         ops += [self.dist.P2POp(self.dist.irecv, self._t(v), peer) for peer, v in recvs]
         if not ops:
-            return
+            return []
         with self.torch.cuda.stream(self.ext):
-            for w in self.dist.batch_isend_irecv(ops):
+            return self.dist.batch_isend_irecv(ops)
+
+    def exchange_finish(self, works):
+        """The solver stream waits for the exchange (device-side wait)."""
+        with self.torch.cuda.stream(self.ext):
+            for w in works:
                 w.wait()
 
 
@@ -388,9 +445,18 @@ class HostStagedComm:
         return out
 
     def exchange(self, sends, recvs):
+        self.exchange_finish(self.exchange_start(sends, recvs))
+
+    def exchange_start(self, sends, recvs):
         reqs = [self.dist.isend(self.torch.from_numpy(self._down(v.ptr, v.n)), p) for p, v in sends]
         bufs = [(v, self.torch.zeros(v.n, dtype=self.torch.float64)) for _, v in recvs]
         reqs += [self.dist.irecv(t, p) for (p, _), (_, t) in zip(recvs, bufs)]
+        return reqs, bufs
+
+    def exchange_finish(self, token):
+        # the halo lands on the stream AFTER whatever was enqueued between
+        # start and finish (the interior SpMV), as with NCCL
+        reqs, bufs = token
         for r in reqs:
             r.wait()
         for v, t in bufs:
@@ -407,15 +473,31 @@ class DistOperator:
         self.plan = HaloPlan.build(bounds, windows, comm.rank)
         self.window = ops.vec(block.window)
         self.own = block.r0 - block.cmin
-        self.mat = ops.prepare(block, cfg)
         # no halo: the window is exactly this rank's rows (one rank, or a
         # block-diagonal matrix), so the SpMV reads the source vector itself
         self.no_halo = not self.plan.recvs and block.window == block.nloc
         self._own = None
+        # interior / boundary split: the interior rows' SpMV overlaps the
+        # halo exchange, the boundary rows follow it
+        self.split = None
+        if (not self.no_halo and self.plan.recvs and hasattr(ops, "prepare_rows")
+                and hasattr(comm, "exchange_start")
+                and os.environ.get("SPMVTUNE_HALO_OVERLAP", "1") != "0"):
+            self.split = interior_rows(block)
+        self._prepare(cfg)
+
+    def _prepare(self, cfg: SpmvConfig):
+        if self.split is None:
+            self.mat, self.parts = self.ops.prepare(self.block, cfg), None
+            return
+        ia, ib = self.split
+        rng = [(ia, ib)] + [(a, b) for a, b in ((0, ia), (ib, self.block.nloc)) if b > a]
+        self.mat = None
+        self.parts = [(a, b - a, self.ops.prepare_rows(self.block, cfg, a, b)) for a, b in rng]
 
     def swap(self, cfg: SpmvConfig):
         self.cfg = cfg
-        self.mat = self.ops.prepare(self.block, cfg)
+        self._prepare(cfg)
 
     def own_view(self):
         """This rank's slice of the window buffer: a vector kept there (CG's
@@ -434,8 +516,16 @@ class DistOperator:
             ops.copy(ops.view(self.window, self.own, b.nloc), ops.view(src, 0, b.nloc))
         sends = [(p, ops.view(src, lo - b.r0, hi - lo)) for p, lo, hi in self.plan.sends]
         recvs = [(p, ops.view(self.window, lo - b.cmin, hi - lo)) for p, lo, hi in self.plan.recvs]
-        self.comm.exchange(sends, recvs)
-        ops.spmv(self.mat, self.cfg, self.window, dst)
+        if self.parts is None:
+            self.comm.exchange(sends, recvs)
+            ops.spmv(self.mat, self.cfg, self.window, dst)
+            return
+        token = self.comm.exchange_start(sends, recvs)
+        (a, cnt, mat), rest = self.parts[0], self.parts[1:]
+        ops.spmv(mat, self.cfg, self.window, ops.view(dst, a, cnt))     # interior: own rows only
+        self.comm.exchange_finish(token)
+        for a, cnt, mat in rest:                                         # boundary rows
+            ops.spmv(mat, self.cfg, self.window, ops.view(dst, a, cnt))
 
 
 # ---------------------------------------------------------------------------
@@ -688,6 +778,7 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
     stream.sync()
     t3 = time.perf_counter()
     res["config"] = cfg.token()
+    res["interior_rows"] = A.split
     if timings is not None:
         timings.update({"predict_s": t1 - t0, "convert_s": t2 - t1, "solve_s": t3 - t2,
                         "total_s": t3 - t0})
@@ -717,5 +808,6 @@ def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=N
     b_local = np.asarray(b[r0:r1], dtype=np.float64)
     res = (dist_cg if method == "cg" else dist_gmres)(A, b_local, params)
     res["config"] = cfg.token()
+    res["interior_rows"] = A.split
     res["x"] = ops.fetch(res["x"])
     return res, bounds

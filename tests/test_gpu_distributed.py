@@ -123,7 +123,7 @@ def _world2_worker(rank, port, method, dims, q):
         res, blk = distributed_stencil_solve(method, dims, offs, w, params, models=models,
                                              comm_class=HostStagedComm)
         q.put((rank, blk.r0, blk.r1, res["iterations"], res["converged"], res["final"],
-               res["x"].to_numpy(), res["config"], blk.cmin, blk.cmax))
+               res["x"].to_numpy(), res["config"], blk.cmin, blk.cmax, res["interior_rows"]))
     except Exception as exc:          # surface worker failures in the parent
         import traceback
         q.put((rank, "error", repr(exc) + traceback.format_exc()[-1500:]))
@@ -148,8 +148,8 @@ def _stencil(dims):
 def test_cuda_path_world2_on_one_gpu(method, dims):
     """World size 2 of the CUDA row-partitioned path (two processes on the
     one GPU, gloo-staged collectives): the halo exchange really moves planes
-    between ranks; iterations within 1 of the oracle and the assembled x
-    matches it."""
+    between ranks, interior rows are multiplied while it is in flight;
+    iterations within 1 of the oracle and the assembled x matches it."""
     import multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -172,8 +172,11 @@ def test_cuda_path_world2_on_one_gpu(method, dims):
     mv = lambda v: O.spmv("CSR/LibB", csr, v)      # noqa: E731
     ref = O.cg(mv, b, tol=1e-8, max_iters=3000) if method == "cg" else \
         O.gmres(mv, b, restart=30, tol=1e-8, max_iters=3000)
-    (_, a0, a1, it0, c0, f0, x0, cfg0, _, cmax0), (_, b0, b1, it1, c1, f1, x1, cfg1, cmin1, _) = out
+    (_, a0, a1, it0, c0, f0, x0, cfg0, _, cmax0, sp0), (_, b0, b1, it1, c1, f1, x1, cfg1, cmin1, _, sp1) = out
     assert a0 == 0 and a1 == b0 and b1 == n and cmax0 >= a1 and cmin1 < b0   # real halos both ways
+    # the interior rows' SpMV ran before the halo landed (HostStagedComm
+    # writes it at exchange_finish), the boundary rows after
+    assert sp0 is not None and sp1 is not None
     assert it0 == it1 and c0 and c1 and f0 == f1 and f0 <= 1e-8
     assert abs(it0 - ref["iterations"]) <= 1
     x = np.concatenate([x0, x1])
@@ -181,3 +184,26 @@ def test_cuda_path_world2_on_one_gpu(method, dims):
     fv = P.extract_features(P.CsrMatrix(n, n, ptr, cols, vals))
     assert cfg0 == cfg1 == P.cascade_predict(
         P.CascadeModelSet.load_dir(os.path.join(os.path.dirname(__file__), "golden", "models")), fv).token()
+
+
+@pytest.mark.parametrize("a,b", [(0, 1), (0, 600), (17, 430), (599, 600), (123, 124)])
+def test_csr_row_slice_is_exact(a, b):
+    """svb_csr_row_slice (the interior/boundary blocks of a rank): the arrays
+    equal the host slice with a rebased row pointer, and the row-local SpMV
+    configurations give exactly the full SpMV's rows."""
+    from paper_2411_10143_b200.formats import CsrMatrix, _new_handle
+    from paper_2411_10143_b200 import _lib
+    n, _, ptr, cols, vals = G.powerlaw_spd(600, seed=3)
+    A = P.CsrMatrix(n, n, ptr, cols, vals)
+    dev = _new_handle(_lib.lib().svb_csr_row_slice, A._device().handle, a, b, None)
+    S = CsrMatrix._wrap(dev)
+    s, e = int(ptr[a]), int(ptr[b])
+    assert (S.nrows, S.ncols, S.nnz) == (b - a, n, e - s)
+    assert np.array_equal(S.row_ptr, ptr[a:b + 1] - s)
+    assert np.array_equal(S.col_idx, cols[s:e]) and np.array_equal(S.values, vals[s:e])
+    x = np.random.default_rng(0).uniform(0.5, 1.5, n)
+    for tok in ("CSR/LibB", "CSR/LibA/4", "CSR/LibA/32"):
+        cfg = P.SpmvConfig.from_token(tok)
+        assert np.array_equal(P.execute_spmv(cfg, S, x), P.execute_spmv(cfg, A, x)[a:b])
+    with pytest.raises(ValueError):
+        _new_handle(_lib.lib().svb_csr_row_slice, A._device().handle, 5, 5, None)
