@@ -173,6 +173,36 @@ int main(int argc, char** argv) {
       printf("%2d: %7.2f..%7.2f | %7.2f..%7.2f | %7.2f..%7.2f | %7.2f..%7.2f\n", p, mn[0], mx[0], mn[1], mx[1],
              mn[2], mx[2], mn[3], mx[3]);
     }
+    // is the spread of the streaming phase (consumed - start) systematic per
+    // CTA (the same SMs slow every pass) or random?
+    std::vector<double> ev(G, 0.0), od(G, 0.0);
+    int ne = 0, no = 0;
+    for (int p = 1; p < np - 1; ++p) {
+      (p & 1 ? no : ne)++;
+      for (int c = 0; c < G; ++c) {
+        const double v = (double)(h[((size_t)c * np + p) * 4 + 1] - h[((size_t)c * np + p) * 4 + 0]) * 1e-3;
+        (p & 1 ? od : ev)[c] += v;
+      }
+    }
+    double me = 0, mo = 0;
+    for (int c = 0; c < G; ++c) { ev[c] /= ne; od[c] /= no; me += ev[c]; mo += od[c]; }
+    me /= G; mo /= G;
+    double sxy = 0, sxx = 0, syy = 0, lo = 1e30, hi = -1e30;
+    for (int c = 0; c < G; ++c) {
+      sxy += (ev[c] - me) * (od[c] - mo); sxx += (ev[c] - me) * (ev[c] - me); syy += (od[c] - mo) * (od[c] - mo);
+      const double a = 0.5 * (ev[c] + od[c]);
+      lo = std::min(lo, a); hi = std::max(hi, a);
+    }
+    printf("stream phase per CTA: mean %.2f us, per-CTA means %.2f..%.2f us, even/odd-pass correlation %.2f\n",
+           0.5 * (me + mo), lo, hi, sxy / sqrt(sxx * syy + 1e-30));
+    std::vector<int> idx(G);
+    for (int c = 0; c < G; ++c) idx[c] = c;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return ev[a] + od[a] > ev[b] + od[b]; });
+    printf("slowest CTAs:");
+    for (int k = 0; k < 12; ++k) printf(" %d(%.2f)", idx[k], 0.5 * (ev[idx[k]] + od[idx[k]]));
+    printf("\nfastest CTAs:");
+    for (int k = G - 12; k < G; ++k) printf(" %d(%.2f)", idx[k], 0.5 * (ev[idx[k]] + od[idx[k]]));
+    printf("\n");
   }
   printf(bad ? "MISMATCH\n" : "ALL OK\n");
   return bad;
