@@ -311,6 +311,56 @@ int svb_forest_destroy(svb_forest* f);
 int svb_forest_predict(const svb_forest* f, const double* x15, double* scores_out,
                        int32_t* label_out);
 
+/* ---- native solver drivers + configuration mailbox -------
+ * svb_gmres_run / svb_cg_run: the whole solve loop of gmres_solve / cg_solve
+ * (solver.py:345-362; reference _gmres_core, solver.py:219-342) in C++ for
+ * hosts without Python.  b_dev/x_dev: device vectors (x0 = 0); A is read,
+ * never modified.  history_host: capacity max_iters doubles (per-iteration
+ * residual estimates); timeline_host: up to timeline_cap swaps, the first
+ * being the initial configuration at iteration 1.  A non-finite scalar
+ * returns SVB_NONFINITE with the reference's message; a breakdown whose
+ * explicit residual stays above tol reports stagnated = 1 (StagnationError).
+ * The mailbox (ConfigMailbox, solver.py:126-185) is polled between
+ * iterations: svb_mailbox_publish (any thread, last writer wins) offers a
+ * matrix handle already stored in cfg.format and an optional CUDA event it
+ * is complete at; a different configuration is swapped in for the next
+ * iteration.  The handle must outlive the solve.  svb_mailbox_finished
+ * reports the solver done (the advisor's cancel flag). */
+typedef struct {
+  int32_t format, library, lane, workers;   /* SpmvConfig + LibC chunk count */
+} svb_config;
+typedef struct {
+  int32_t restart_m;   /* GMRES(m); ignored by CG */
+  int32_t max_iters;
+  double tol;
+} svb_solve_params;
+typedef struct {
+  int32_t iteration;   /* first iteration run with `config` */
+  svb_config config;
+  double prep_seconds;
+} svb_swap;
+typedef struct {
+  int32_t converged;
+  int32_t stagnated;
+  int32_t iterations;
+  int32_t history_len;
+  int32_t nswaps;         /* timeline entries (may exceed timeline_cap) */
+  double final_residual;  /* NaN when max_iters == 0 (reference: None) */
+} svb_solve_report;
+typedef struct svb_mailbox svb_mailbox;
+int svb_mailbox_create(svb_mailbox** out);
+int svb_mailbox_destroy(svb_mailbox* mb);
+int svb_mailbox_publish(svb_mailbox* mb, const svb_matrix* m, svb_config cfg, void* ready_event,
+                        double prep_seconds);
+int svb_mailbox_finished(svb_mailbox* mb, int32_t* out);
+int svb_gmres_run(const svb_matrix* A, svb_config cfg, const double* b_dev, double* x_dev,
+                  const svb_solve_params* params, svb_mailbox* mb, void* stream, double* history_host,
+                  svb_swap* timeline_host, int32_t timeline_cap, svb_solve_report* out);
+int svb_cg_run(const svb_matrix* A, svb_config cfg, const double* b_dev, double* x_dev,
+               const svb_solve_params* params, svb_mailbox* mb, void* stream, double* history_host,
+               svb_swap* timeline_host, int32_t timeline_cap, svb_solve_report* out);
+
+
 #ifdef __cplusplus
 }
 #endif

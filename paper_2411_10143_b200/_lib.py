@@ -46,6 +46,24 @@ class KrylovStatus(C.Structure):
                 ("done", C.c_int32), ("count", C.c_int64)]
 
 
+class SvbConfig(C.Structure):
+    _fields_ = [("format", C.c_int32), ("library", C.c_int32), ("lane", C.c_int32),
+                ("workers", C.c_int32)]
+
+
+class SolveParams(C.Structure):
+    _fields_ = [("restart_m", C.c_int32), ("max_iters", C.c_int32), ("tol", C.c_double)]
+
+
+class Swap(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("config", SvbConfig), ("prep_seconds", C.c_double)]
+
+
+class SolveReportC(C.Structure):
+    _fields_ = [("converged", C.c_int32), ("stagnated", C.c_int32), ("iterations", C.c_int32),
+                ("history_len", C.c_int32), ("nswaps", C.c_int32), ("final_residual", C.c_double)]
+
+
 # name -> argtypes (all functions return int status unless listed in _RESTYPE)
 _SIGS = {
     "svb_last_error": [],
@@ -91,6 +109,14 @@ _SIGS = {
     "svb_graph_launch": [_P, _P],
     "svb_graph_destroy": [_P],
     "svb_csr_row_slice": [_P, C.c_int64, C.c_int64, _P, _PP],
+    "svb_mailbox_create": [_PP],
+    "svb_mailbox_destroy": [_P],
+    "svb_mailbox_publish": [_P, _P, SvbConfig, _P, C.c_double],
+    "svb_mailbox_finished": [_P, C.POINTER(C.c_int32)],
+    "svb_gmres_run": [_P, SvbConfig, _P, _P, C.POINTER(SolveParams), _P, _P, _PD, C.POINTER(Swap),
+                      C.c_int32, C.POINTER(SolveReportC)],
+    "svb_cg_run": [_P, SvbConfig, _P, _P, C.POINTER(SolveParams), _P, _P, _PD, C.POINTER(Swap),
+                   C.c_int32, C.POINTER(SolveReportC)],
     "svb_csr_stencil_rows": [C.c_int, _PI64, C.c_int, C.POINTER(C.c_int32), _PD, C.c_int64, C.c_int64,
                              C.c_int64, C.c_int64, _P, _PP],
     "svb_convert": [_P, C.c_int, _I64, _P, _PP],

@@ -36,6 +36,7 @@ SOURCES = {
     "generate.cu": [],
     "forest.cpp": [],
     "mmio.cu": [],
+    "driver.cu": [],
 }
 
 

@@ -195,3 +195,25 @@ def test_no_oracle_import_in_product():
     for p in (ROOT / "paper_2411_10143_b200").rglob("*.py"):
         text = p.read_text()
         assert "import oracle" not in text and "from oracle" not in text, p
+
+
+def test_native_mailbox_and_driver_argument_checks_on_host():
+    """The C-ABI mailbox needs no GPU; the native drivers reject bad
+    arguments before touching the device."""
+    import ctypes
+    from paper_2411_10143_b200 import _lib
+    mb = P.NativeMailbox()
+    assert mb.finished is False
+    L = _lib.load()
+    rep = _lib.SolveReportC()
+    sp = _lib.SolveParams(30, 10, 1e-8)
+    st = L.svb_gmres_run(None, _lib.SvbConfig(1, 1, 0, 1), None, None, ctypes.byref(sp), None, None,
+                         None, None, 0, ctypes.byref(rep))
+    assert st == _lib.INVALID and "null argument" in _lib.last_error()
+    sp0 = _lib.SolveParams(0, 10, 1e-8)
+    st = L.svb_gmres_run(None, _lib.SvbConfig(1, 1, 0, 1), None, None, ctypes.byref(sp0), None, None,
+                         None, None, 0, ctypes.byref(rep))
+    assert st == _lib.INVALID and "restart_m" in _lib.last_error()
+    with pytest.raises(ValueError):
+        P.native_solve("bicgstab", None)
+    del mb
