@@ -51,6 +51,48 @@ __device__ void block_reduce_store(FeatAcc a, FeatAcc* out) {
   }
 }
 
+// Rows longer than FEAT_LONG entries are handed to a warp: one thread
+// walking a power-law row of thousands of entries (a dependent bitmap probe
+// per entry) would otherwise set the kernel time on its own.
+constexpr int FEAT_LONG = 64;
+
+// Longest run of consecutive columns and the diagonal marks of one row by a
+// warp, in the sequential recurrence's terms (run = c == prev + 1 ? run + 1
+// : 1, best = max run); returns (best, last - first column) on every lane.
+template <class G>
+__device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e, int64_t diag0,
+                                              unsigned* __restrict__ bits, long long* dcache,
+                                              long long* best_out, long long* span_out) {
+  const int lane = threadIdx.x & 31;
+  long long best = 0, carry = 0;   // run length through the previous chunk's last entry
+  int prev_last = 0;
+  const int first = col(s);
+  int last = first;
+  for (int64_t base = s; base < e; base += 32) {
+    const int64_t k = base + lane;
+    const bool valid = k < e;
+    const int c = valid ? col(k) : 0;
+    int pc = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane == 0) pc = prev_last;
+    const bool brk = valid && ((k == s) || c != pc + 1);
+    if (valid) mark_diag(bits, (long long)c + diag0, dcache);
+    const unsigned B = __ballot_sync(0xffffffffu, brk);
+    const unsigned upto = B & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+    long long run = 0;
+    if (valid) run = upto ? (long long)(lane - (31 - __clz(upto)) + 1) : carry + lane + 1;
+    long long m = run;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, (long long)__shfl_xor_sync(0xffffffffu, m, o));
+    best = max(best, m);
+    const int nv = (int)(e - base < 32 ? e - base : 32);
+    carry = __shfl_sync(0xffffffffu, run, nv - 1);
+    prev_last = __shfl_sync(0xffffffffu, c, nv - 1);
+    last = prev_last;
+  }
+  *best_out = best;
+  *span_out = (long long)last - first;
+}
+
 template <class P, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __restrict__ ptr,
                                                     const int* __restrict__ cols,
@@ -58,34 +100,55 @@ __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __re
   constexpr int CAP = 8192;  // staged column indices per tile (32 KB)
   __shared__ int scol[CAP];
   __shared__ long long dcache[DIAG_CACHE];
+  __shared__ int lrows[BLOCK];
+  __shared__ int nl;
   diag_cache_init(dcache);   // (the tile loop's first __syncthreads orders it)
+  if (threadIdx.x == 0) nl = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
   const int64_t ntiles = (nrows + BLOCK - 1) / BLOCK;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const StagedRows<P> t = stage_row_tile<P, BLOCK, CAP>(tile, nrows, ptr, cols, scol);
-    const int64_t i = t.r0 + threadIdx.x;
-    if (i >= t.r1) continue;
-    const int64_t s = (int64_t)ptr[i] - t.base, e = (int64_t)ptr[i + 1] - t.base, L = e - s;
     auto col = [&](int64_t k) { return t.staged ? scol[k] : __ldg(cols + t.base + k); };
-    a.sum_r += (unsigned long long)L;
-    a.sum_r2 += (unsigned long long)(L * L);
-    a.max_r = max(a.max_r, (long long)L);
-    a.min_r = min(a.min_r, (long long)L);
-    if (L == 0) continue;
-    const int64_t diag0 = nrows - 1 - i;
-    const int c0 = col(s);
-    int prev = c0;
-    int64_t run = 1, best = 1;
-    for (int64_t k = s;;) {
-      mark_diag(bits, (long long)prev + diag0, dcache);
-      if (++k >= e) break;
-      const int c = col(k);
-      run = (c == prev + 1) ? run + 1 : 1;
-      best = max(best, run);
-      prev = c;
+    const int64_t i = t.r0 + threadIdx.x;
+    if (i < t.r1) {
+      const int64_t s = (int64_t)ptr[i] - t.base, e = (int64_t)ptr[i + 1] - t.base, L = e - s;
+      a.sum_r += (unsigned long long)L;
+      a.sum_r2 += (unsigned long long)(L * L);
+      a.max_r = max(a.max_r, (long long)L);
+      a.min_r = min(a.min_r, (long long)L);
+      if (L > FEAT_LONG) {
+        lrows[atomicAdd(&nl, 1)] = threadIdx.x;
+      } else if (L > 0) {
+        const int64_t diag0 = nrows - 1 - i;
+        const int c0 = col(s);
+        int prev = c0;
+        int64_t run = 1, best = 1;
+        for (int64_t k = s;;) {
+          mark_diag(bits, (long long)prev + diag0, dcache);
+          if (++k >= e) break;
+          const int c = col(k);
+          run = (c == prev + 1) ? run + 1 : 1;
+          best = max(best, run);
+          prev = c;
+        }
+        a.span += (unsigned long long)(prev - c0);
+        a.runs += (unsigned long long)best;
+      }
     }
-    a.span += (unsigned long long)(prev - c0);
-    a.runs += (unsigned long long)best;
+    __syncthreads();
+    for (int q = warp; q < nl; q += BLOCK / 32) {
+      const int64_t r = t.r0 + lrows[q];
+      const int64_t s = (int64_t)ptr[r] - t.base, e = (int64_t)ptr[r + 1] - t.base;
+      long long best, span;
+      warp_row_runs(col, s, e, nrows - 1 - r, bits, dcache, &best, &span);
+      if (lane == 0) {
+        a.span += (unsigned long long)span;
+        a.runs += (unsigned long long)best;
+      }
+    }
+    __syncthreads();   // every warp is done with nl / lrows
+    if (threadIdx.x == 0) nl = 0;
   }
   block_reduce_store<BLOCK>(a, out);
 }

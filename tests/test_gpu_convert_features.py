@@ -137,3 +137,36 @@ def test_device_stencil_generator_matches_host():
         assert np.array_equal(dev.row_ptr, ptr)
         assert np.array_equal(dev.col_idx, cols)
         assert np.array_equal(dev.values, vals)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_features_long_rows_warp_path(seed):
+    """Rows longer than the per-thread limit (k_features hands them to a
+    warp): runs of consecutive columns crossing 32-entry chunk boundaries,
+    runs that start a row, single-entry gaps, very long dense rows and empty
+    rows between them — aggregates equal the oracle's exactly."""
+    rng = np.random.default_rng(seed)
+    n = 3000
+    rows = []
+    for i in range(n):
+        kind = rng.integers(0, 5)
+        if kind == 0:
+            rows.append(np.array([], dtype=np.int64))
+        elif kind == 1:                          # short random row
+            rows.append(np.unique(rng.integers(0, n, size=rng.integers(1, 20))))
+        elif kind == 2:                          # long row of consecutive blocks
+            starts = np.sort(rng.choice(n - 200, size=rng.integers(2, 6), replace=False))
+            blk = [np.arange(s0, s0 + rng.integers(1, 150)) for s0 in starts]
+            rows.append(np.unique(np.concatenate(blk)))
+        elif kind == 3:                          # very long random row
+            rows.append(np.unique(rng.integers(0, n, size=rng.integers(65, 1500))))
+        else:                                    # one long consecutive run
+            s0 = int(rng.integers(0, n - 700))
+            rows.append(np.arange(s0, s0 + int(rng.integers(60, 700))))
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([r.size for r in rows])
+    cols = np.concatenate(rows).astype(np.int64)
+    vals = np.ones(cols.size)
+    A = P.CsrMatrix(n, n, ptr, cols, vals)
+    got = P.extract_features(A)
+    assert got.to_array().tolist() == O.features(O.OCsr(n, n, ptr, cols, vals))
