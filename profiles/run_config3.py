@@ -34,12 +34,16 @@ out = {"models": os.environ.get("MODELS", "shipped"), "workload": f"config3: CG 
 fv = P.extract_features(A)
 out["features"] = {k: getattr(fv, k) for k in ("mean", "sd", "cov", "max", "ndiag", "diagfill")}
 out["cascade"] = P.cascade_predict(models, fv).token()
+# b computed once, outside every clock (the reference times solves with b
+# given: solver.py:355-358, 470-471, 508-510)
+from paper_2411_10143_b200.solver import default_rhs  # noqa: E402
+bvec = default_rhs(A, params)
 with DeviceOptions(keep_solution_on_device=True):
-    P.async_solve(A, None, params, models, method="cg", initial_config=start)      # warm-up
+    P.async_solve(A, bvec, params, models, method="cg", initial_config=start)      # warm-up
     runs = []
     for _ in range(3):
         t = time.perf_counter()
-        r = P.async_solve(A, None, params, models, method="cg", initial_config=start)
+        r = P.async_solve(A, bvec, params, models, method="cg", initial_config=start)
         runs.append(time.perf_counter() - t)
     out["async_s"] = sorted(runs)[1]
     out["async_iterations"] = r.iterations
@@ -49,13 +53,13 @@ with DeviceOptions(keep_solution_on_device=True):
     dts, sts = [], []
     for _ in range(3):
         t = time.perf_counter()
-        d = P.cg_solve(A, None, params, initial_config=start)
+        d = P.cg_solve(A, bvec, params, initial_config=start)
         dts.append(time.perf_counter() - t)
     out["default_csr_vector_s"] = sorted(dts)[1]
     out["default_iterations"] = d.iterations
     for _ in range(3):
         t = time.perf_counter()
-        s = P.sequential_predict_solve(A, None, params, models, method="cg")
+        s = P.sequential_predict_solve(A, bvec, params, models, method="cg")
         sts.append((time.perf_counter() - t, s.phases))
     sts.sort(key=lambda e: e[0])
     out["sequential_s"], out["sequential_phases"] = sts[1]
