@@ -281,18 +281,35 @@ constexpr int TILE_ROWS = 256;
 __global__ void __launch_bounds__(TILE_ROWS) k_diag_bits(int64_t nrows, const int64_t* __restrict__ ptr,
                                                          const int* __restrict__ cols, unsigned* __restrict__ bits) {
   constexpr int CAP = 8192;
+  constexpr int LONG = 64;   // longer rows are marked by a warp (power-law tails)
   __shared__ int scol[CAP];
   __shared__ long long dcache[DIAG_CACHE];
+  __shared__ int lrows[TILE_ROWS];
+  __shared__ int nl;
   diag_cache_init(dcache);
+  if (threadIdx.x == 0) nl = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (nrows + TILE_ROWS - 1) / TILE_ROWS;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const StagedRows<int64_t> t = stage_row_tile<int64_t, TILE_ROWS, CAP>(tile, nrows, ptr, cols, scol);
+    auto col = [&](int64_t k) { return t.staged ? scol[k] : __ldg(cols + t.base + k); };
     const int64_t i = t.r0 + threadIdx.x;
-    if (i >= t.r1) continue;
-    for (int64_t k = ptr[i] - t.base, e = ptr[i + 1] - t.base; k < e; ++k) {
-      const int c = t.staged ? scol[k] : __ldg(cols + t.base + k);
-      mark_diag(bits, (long long)c - i + nrows - 1, dcache);
+    if (i < t.r1) {
+      const int64_t s0 = ptr[i] - t.base, e = ptr[i + 1] - t.base;
+      if (e - s0 > LONG) {
+        lrows[atomicAdd(&nl, 1)] = threadIdx.x;
+      } else {
+        for (int64_t k = s0; k < e; ++k) mark_diag(bits, (long long)col(k) - i + nrows - 1, dcache);
+      }
     }
+    __syncthreads();
+    for (int q = warp; q < nl; q += TILE_ROWS / 32) {
+      const int64_t r = t.r0 + lrows[q];
+      for (int64_t k = ptr[r] - t.base + lane, e = ptr[r + 1] - t.base; k < e; k += 32)
+        mark_diag(bits, (long long)col(k) - r + nrows - 1, dcache);
+    }
+    __syncthreads();   // every warp is done with nl / lrows
+    if (threadIdx.x == 0) nl = 0;
   }
 }
 

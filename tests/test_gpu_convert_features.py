@@ -170,3 +170,18 @@ def test_features_long_rows_warp_path(seed):
     A = P.CsrMatrix(n, n, ptr, cols, vals)
     got = P.extract_features(A)
     assert got.to_array().tolist() == O.features(O.OCsr(n, n, ptr, cols, vals))
+
+
+@pytest.mark.parametrize("nd", [70, 300, 1200])
+def test_dia_conversion_long_rows_warp_path(nd):
+    """Banded rows longer than 64 entries (the diagonal bitmap marks them by
+    a warp): the DIA offsets and data equal the oracle conversion exactly."""
+    rng = np.random.default_rng(nd)
+    n = 4000
+    offs = np.unique(np.concatenate([[0], rng.integers(-1500, 1501, size=nd)]))
+    nn, _, ptr, cols, vals = G.banded(n, offs.tolist(), seed=nd, diagonal_boost=2.0 * len(offs))
+    A = P.CsrMatrix(nn, nn, ptr, cols, vals)
+    D = P.convert(A, P.FormatTag.DIA)
+    ref = O.convert(O.OCsr(nn, nn, ptr, cols, vals), "DIA")
+    assert np.array_equal(np.asarray(D.offsets), np.asarray(ref.offsets))
+    assert np.array_equal(np.asarray(D.data), np.asarray(ref.data))
