@@ -707,12 +707,24 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_tmem(Gm G, int j, double bnorm
 // ~1K flops, from H in L2), which replaces a separate one-thread launch.
 __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restrict__ x) {
   __shared__ double ys[64];
+  __shared__ double hs[32 * 32 + 32];   // the (j+1)^2 triangle of H and g, staged once
+  const int m = G.m, nj = j + 1;
+  if (nj <= 32) {
+    for (int t = threadIdx.x; t < nj * nj; t += blockDim.x) hs[t] = G.H[(t / nj) * m + (t % nj)];
+    for (int t = threadIdx.x; t < nj; t += blockDim.x) hs[nj * nj + t] = G.g[t];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int m = G.m;
+    // back substitution in the reference order (solver.py:211-214)
     for (int i = j; i >= 0; --i) {
       double dot = 0.0;
-      for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * ys[k];
-      ys[i] = (G.g[i] - dot) / G.H[i * m + i];
+      if (nj <= 32) {
+        for (int k = i + 1; k <= j; ++k) dot += hs[i * nj + k] * ys[k];
+        ys[i] = (hs[nj * nj + i] - dot) / hs[i * nj + i];
+      } else {
+        for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * ys[k];
+        ys[i] = (G.g[i] - dot) / G.H[i * m + i];
+      }
     }
     if (blockIdx.x == 0)
       for (int i = 0; i <= j; ++i) G.y[i] = ys[i];
@@ -722,7 +734,18 @@ __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restr
       G.n,
       [&](int64_t e) {
         double2 t = make_double2(0.0, 0.0);
-        for (int i = 0; i <= j; ++i) {
+        int i = 0;
+        for (; i + 8 <= nj; i += 8) {   // 8 rows' loads in flight, summed in row order
+          double2 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = ld2(G.V + (int64_t)(i + u) * G.ld + e);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            t.x += v[u].x * ys[i + u];
+            t.y += v[u].y * ys[i + u];
+          }
+        }
+        for (; i <= j; ++i) {
           double2 v = ld2(G.V + (int64_t)i * G.ld + e);
           t.x += v.x * ys[i];
           t.y += v.y * ys[i];
