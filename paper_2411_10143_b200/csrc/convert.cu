@@ -426,12 +426,20 @@ static svb_matrix* build_ell(const RowView& v, int64_t max_cells, cudaStream_t s
   return m;
 }
 
-static svb_matrix* build_dia(const RowView& v, cudaStream_t s) {
+static svb_matrix* build_dia(const RowView& v, const svb_matrix* src, cudaStream_t s) {
   const int64_t nbits = v.nrows + v.ncols - 1;
   const int64_t nwords = (nbits + 31) / 32;
-  Buf bits = alloc(nwords * 4, s);
-  SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
-  if (v.nnz) {
+  Buf bits;
+  if (src->fmt == SVB_CSR) {   // the bitmap feature extraction left on the handle
+    std::lock_guard<std::mutex> lk(src->mu);
+    if (src->diag_bits && src->diag_bits->bytes >= (size_t)nwords * 4) bits = src->diag_bits;
+  }
+  const bool reused = (bool)bits;
+  if (!reused) {
+    bits = alloc(nwords * 4, s);
+    SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
+  }
+  if (v.nnz && !reused) {
     k_diag_bits<<<grid_for(v.nrows, TILE_ROWS), TILE_ROWS, 0, s>>>(v.nrows, ptr<int64_t>(v.ptr), ptr<int>(v.cols),
                                                        ptr<unsigned>(bits));
     SVB_CHECK_LAUNCH();
@@ -527,7 +535,7 @@ int svb_convert(const svb_matrix* src, int target, int64_t max_ell_cells, void* 
       case SVB_COO: m = build_coo(v, src, s); break;
       case SVB_CSR: m = build_csr(v, s); break;
       case SVB_ELL: m = build_ell(v, max_ell_cells, s); break;
-      case SVB_DIA: m = build_dia(v, s); break;
+      case SVB_DIA: m = build_dia(v, src, s); break;
       default: m = build_hyb(v, s); break;
     }
     SVB_CUDA_TRY(cudaStreamSynchronize(s));

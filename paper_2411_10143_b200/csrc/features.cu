@@ -205,6 +205,11 @@ extern "C" int svb_features(const svb_matrix* m, int64_t* agg, void* stream) {
     } h;
     SVB_CUDA_TRY(cudaMemcpyAsync(&h, acc->ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    {  // complete now: kept for a later DIA conversion of this handle
+      detach(bits);
+      std::lock_guard<std::mutex> lk(m->mu);
+      m->diag_bits = bits;
+    }
     agg[0] = (int64_t)h.a.sum_r;
     agg[1] = (int64_t)h.a.sum_r2;
     agg[2] = h.a.max_r;

@@ -46,6 +46,9 @@ struct svb_matrix {
   // the spill kernel never tiles the rows that spill nothing
   mutable int64_t nhruns = -1;
   mutable svb::Buf hruns, hmap;
+  // CSR: the diagonal-occupancy bitmap svb_features built (bit c - i + n - 1),
+  // reused by the DIA conversion instead of a second pass over col_idx
+  mutable svb::Buf diag_bits;
 
   int64_t device_bytes() const {
     int64_t b = 0;
