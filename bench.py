@@ -111,7 +111,7 @@ def reference_arm(args):
         metric, workload = METRIC, WORKLOAD
     line = {"metric": metric, "value": r["value"], "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"] * 1e3,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": workload, "mode": "sequential predict-then-solve (CPU)"},
             "cpu_baseline": {"value": r["value"], "unit": "s", "cores": r["cores"],
@@ -560,7 +560,8 @@ def b200_arm(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                # one fixed system at every N (N > 1: row-partitioned, dist_arm)
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "mode": "async",
                            "parallelism": f"replicas{ws}" if ws > 1 else "single",
                            "l2": "inputs larger than L2 (CSR 448 MB + Krylov basis 992 MB vs 126 MB L2)"},
