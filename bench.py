@@ -1,29 +1,32 @@
-"""Benchmark: GMRES(30) time-to-solution including preprocessing on B200.
+"""Benchmark: CG time-to-solution including preprocessing, row-partitioned, on B200.
 
-Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
-GMRES(30), fp64, tol 1e-8, b = A*1, on the nonsymmetric 9-point
-convection-diffusion matrix 2000x2000 (n = 4,000,000, nnz = 35,976,004).
-One step = one full async predict-while-solve (the paper's AsyGMRES): the
-solve starts at once on the default CSR-vector kernel (CSR/LibA/32) while
-the advisor stream extracts features, runs the shipped cascade models and
-converts to the predicted format; the solver swaps mid-solve.  Time to
-solution therefore includes all preprocessing.
+Workload (every N): BASELINE.json configs[4], the largest configuration that
+fits one GPU and the north star's scaling target — CG fp64, tol 1e-8,
+b = A*1, on the 3-D 27-point Laplacian 600^3 (n = 216,000,000,
+nnz = 5,812,581,592), rows split into z-slabs across N ranks (N = 1: one
+slab).  One step = the reference's predict-then-solve flow (solver.py:
+496-540) on the row-partitioned operator: exact global features -> cascade
+(the reference's shipped models) -> conversion of each rank's slab to the
+predicted format -> CG with NCCL halo exchange + scalar all-reduces.  The
+same code path runs at N = 1, 2, 4, 8 (strong scaling: the problem is fixed).
 
-  value  — seconds per solve with the matrix and b resident in HBM
-  e2e    — the same solve through the public API from pinned HOST buffers:
-           CSR upload (H2D) inside the clock, solution download (D2H)
-  roofline — the dominant kernel group of the step, bytes per §8(d),
-           timed with CUDA events on the solver stream inside the timed steps
-  cpu_baseline — the reference algorithm (oracle port, bit-exact to the
-           reference) on the host cores, bounded sample (oracle/bench_cpu.py)
+  value   — seconds per solve, slabs generated in HBM before the clock
+  e2e     — the same solve through distributed_solve_slab from each rank's
+            PINNED HOST slab (row_ptr int64, global col_idx int32, values f64,
+            b): upload + device validation inside the clock, x back to host
+  roofline — the dominant kernel (the local SpMV in the predicted format),
+            algorithmic bytes per SURVEY §8(d) / its average launch time
+            from CUDA events on the solver stream over one instrumented solve
+  cpu_baseline — the reference algorithm (oracle port) on the host cores,
+            bounded 120^3 sample scaled per nnz (the 600^3 matrix does not fit
+            the host), with a 150^3 / 300^3 linearity check in the reference arm
+  detail  — (N = 1) config 2 (GMRES(30) async predict-while-solve, 4 M rows,
+            e2e, default CSR-vector and sequential), config 1 (CG Poisson
+            1024^2) and config 3 (CG power-law 8 M rows) on one B200
 
+`python bench.py --gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks; under torchrun WORLD_SIZE must equal N.
 `--impl reference` prints the reference arm (CPU oracle port) instead.
-Multi-GPU (torchrun, N > 1): the row-partitioned solver (distributed.py) on
-the same config-2 problem — each rank generates its slab on its GPU, the
-cascade runs on exact global features, SpMV halos and dot products go over
-NCCL (strong scaling, value = max over ranks).  `--workload config5` runs
-BASELINE configs[4] (row-partitioned CG, 27-point Laplacian 600^3) the same
-way at any N, including N = 1.
 """
 from __future__ import annotations
 
@@ -31,6 +34,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,23 +49,32 @@ sys.path.insert(0, str(ROOT))
 # launch must not land inside a timed step
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
-NX = 2000
 TOL = 1e-8
+N3 = int(os.environ.get("SPMVTUNE_CONFIG5_N", "600"))
+NX2 = 2000
 RESTART = 30
-METRIC = "GMRES(30) time-to-solution incl. preprocessing (features+cascade+conversion)"
-METRIC5 = "CG time-to-solution incl. preprocessing (features+cascade+conversion)"
-WORKLOAD = (f"config2: GMRES({RESTART}) fp64, tol {TOL:g}, b=A*1, nonsymmetric 9-point "
-            f"convection-diffusion {NX}x{NX} (n={NX * NX:,}, nnz={(3 * NX - 2) ** 2:,}); async "
-            "predict-while-solve starting on CSR/LibA/32 with the reference's shipped cascade "
-            "models")
+METRIC = "CG time-to-solution incl. preprocessing (features+cascade+conversion)"
+METRIC2 = "GMRES(30) time-to-solution incl. preprocessing (features+cascade+conversion)"
+
+
+def workload5(n3: int = N3) -> str:
+    return (f"config5: CG fp64, tol {TOL:g}, b=A*1, 3-D 27-point Laplacian {n3}^3 "
+            f"(n={n3 ** 3:,}, nnz={(3 * n3 - 2) ** 3:,}); row-partitioned z-slabs, predict-then-solve "
+            "(exact global features -> shipped cascade models -> per-rank conversion), NCCL halo + "
+            "all-reduce; the same code path at every N")
+
+
+WORKLOAD2 = (f"config2: GMRES({RESTART}) fp64, tol {TOL:g}, b=A*1, nonsymmetric 9-point "
+             f"convection-diffusion {NX2}x{NX2} (n={NX2 * NX2:,}, nnz={(3 * NX2 - 2) ** 2:,}); async "
+             "predict-while-solve starting on CSR/LibA/32 with the reference's shipped cascade models")
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
@@ -71,55 +84,95 @@ def dist_env():
     return ws, rank, local
 
 
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without torchrun: run this script under torch.distributed.run
+    with N ranks (one per GPU) and pass its output and exit code through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the CPU oracle port on the host cores
 # ---------------------------------------------------------------------------
-def run_cpu_sample(steps: int, warmup: int, total_iters: int, iters: int = 8) -> dict:
+def _oracle_env():
     env = dict(os.environ)
     env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
     env.pop("CUDA_VISIBLE_DEVICES", None)
-    cmd = [sys.executable, "-m", "oracle.bench_cpu", "--nx", str(NX), "--iters", str(iters),
-           "--total-iters", str(total_iters), "--repeat", str(steps), "--warmup", str(warmup)]
-    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
-    if out.returncode != 0:
-        raise RuntimeError(out.stderr[-2000:])
-    return json.loads(out.stdout.strip().splitlines()[-1])
+    return env
+
+
+def run_oracle(args_list, timeout=1800) -> dict:
+    o = subprocess.run([sys.executable, "-m", "oracle.bench_cpu", *args_list], cwd=ROOT, env=_oracle_env(),
+                       capture_output=True, text=True, timeout=timeout)
+    if o.returncode != 0:
+        raise RuntimeError(o.stderr[-2000:])
+    return json.loads(o.stdout.strip().splitlines()[-1])
+
+
+def cpu_config5_sample(total_iters: int, n3: int = 120, iters: int = 4) -> dict:
+    return run_oracle(["--laplace27", str(n3), "--iters", str(iters), "--total-iters", str(total_iters),
+                       "--target", str(N3)])
 
 
 def reference_arm(args):
+    """The reference's CPU path (oracle port, bit-exact to /root/reference)
+    on the host cores, same workload, metric and unit as the B200 arm.  The
+    600^3 matrix (94.7 GB as int64 CSR) does not fit the host's RAM next to
+    its conversions, so each step is a bounded 120^3 sample of the
+    predict-then-solve flow, scaled per nnz (EXTRAPOLATED — labelled); a
+    150^3 and a 300^3 sample check that per-nnz scaling is linear; config 2
+    runs in full (async flow, measured, not extrapolated) in `detail`."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     t0 = time.perf_counter()
-    if args.workload == "config5":
-        # the 600^3 matrix does not fit the host: a 120^3 sample, extrapolated
-        env = dict(os.environ)
-        env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
-        env.pop("CUDA_VISIBLE_DEVICES", None)
-        vals = []
-        for _ in range(args.warmup + args.steps):
-            o = subprocess.run([sys.executable, "-m", "oracle.bench_cpu", "--laplace27", "120", "--iters", "4",
-                                "--total-iters", "763", "--target", "600"], cwd=ROOT, env=env,
-                               capture_output=True, text=True, timeout=1800)
-            vals.append(json.loads(o.stdout.strip().splitlines()[-1]))
-        r = vals[-1]
-        r["values"] = [v["value"] for v in vals[args.warmup:]]
-        r["value"] = statistics.median(r["values"])
-        metric, workload = METRIC5, stencil_problem("config5")[4]
-    else:
-        r = run_cpu_sample(args.steps, args.warmup, args.total_iters)
-        metric, workload = METRIC, WORKLOAD
-    line = {"metric": metric, "value": r["value"], "unit": "s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["value"] * 1e3,
+    total_iters = args.total_iters
+    vals, last = [], None
+    for k in range(args.warmup + args.steps):
+        last = cpu_config5_sample(total_iters)
+        if k >= args.warmup:
+            vals.append(last["value"])
+    value = statistics.median(vals)
+    detail = {"per_step_values": vals, "phases": last["phases"], "config": last["config"],
+              "per_iteration_s_extrapolated": last["per_iteration_s"], "total_iterations": total_iters}
+    if not args.no_extra:
+        lin = {}
+        for n3 in (150, 300):
+            try:
+                r = cpu_config5_sample(total_iters, n3=n3, iters=2)
+                lin[f"{n3}^3"] = {"extrapolated_s": r["value"], "per_iteration_s": r["per_iteration_s"],
+                                  "sampled_nnz": r.get("sampled_nnz")}
+            except Exception as exc:
+                lin[f"{n3}^3"] = f"failed: {exc}"[:300]
+        if all(isinstance(v, dict) for v in lin.values()):
+            a, b = lin["150^3"]["extrapolated_s"], lin["300^3"]["extrapolated_s"]
+            lin["ratio_300_over_150"] = b / a     # 1.0 = per-nnz scaling is linear
+        detail["linearity_check"] = lin
+        try:
+            detail["config2_cpu_async_measured"] = run_oracle(["--nx", str(NX2), "--async-full"], timeout=1200)
+        except Exception as exc:
+            detail["config2_cpu_async_measured"] = f"failed: {exc}"[:300]
+    detail["wall_seconds"] = time.perf_counter() - t0
+    line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload, "mode": "sequential predict-then-solve (CPU)"},
-            "cpu_baseline": {"value": r["value"], "unit": "s", "cores": r["cores"],
-                             "kind": r["kind"], "sample": r["sample"]},
-            "e2e": {"value": r["value"], "unit": "s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-            "detail": {"phases": r["phases"], "values": r.get("values"), "config": r["config"],
-                       "wall_seconds": time.perf_counter() - t0}}
+            "config": {"workload": workload5(), "mode": "predict-then-solve (CPU, reference algorithm)"},
+            "cpu_baseline": {"value": value, "unit": "s", "cores": last["cores"], "kind": last["kind"],
+                             "sample": last["sample"], "cpu_model": last.get("cpu_model")},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "extrapolated": True,
+            "detail": detail}
     print(json.dumps(line), flush=True)
 
 
@@ -127,7 +180,8 @@ def reference_arm(args):
 # measurement helpers
 # ---------------------------------------------------------------------------
 class EventTimer:
-    """CUDA-event pairs around solver launches, recorded on the solver stream."""
+    """CUDA-event pairs around solver launches, recorded on the launching
+    stream (the solver's own stream, not torch's current one)."""
 
     def __init__(self):
         import torch
@@ -135,7 +189,6 @@ class EventTimer:
         self.streams = {}
         self.open = {}
         self.done = []
-        self.active = False
 
     def _stream(self, h):
         s = self.streams.get(h)
@@ -144,15 +197,11 @@ class EventTimer:
         return s
 
     def begin(self, tag, h):
-        if not self.active:
-            return
         ev = self.torch.cuda.Event(enable_timing=True)
         ev.record(self._stream(h))
         self.open[tag] = ev
 
     def end(self, tag, h):
-        if not self.active:
-            return
         ev = self.torch.cuda.Event(enable_timing=True)
         ev.record(self._stream(h))
         self.done.append((tag, self.open.pop(tag), ev))
@@ -216,6 +265,8 @@ class NvmlClockSampler:
 
 
 class ClockSampler:
+    """nvidia-smi fallback when NVML is unavailable."""
+
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -234,33 +285,34 @@ class ClockSampler:
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = []
-        for line in Path(self.f.name).read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                rows.append(parts)
+        rows = [[x.strip() for x in line.split(",")] for line in Path(self.f.name).read_text().splitlines()]
+        rows = [r for r in rows if len(r) >= 8]
         os.unlink(self.f.name)
         loaded = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
         sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
-        reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in loaded:
-            for k, name in enumerate(names):
-                if r[3 + k].lower() == "active":
-                    reasons.add(name)
+        reasons = {name for r in loaded for k, name in enumerate(names) if r[3 + k].lower() == "active"}
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(loaded[0][1]) if loaded else None,
                 "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(loaded)}
 
 
-def algorithmic_bytes(tag: str, info, n: int) -> float:
-    """Bytes per launch per SURVEY.md §8(d) (device layout: fp64 values,
-    int32 indices)."""
-    tok = tag.split(":", 1)[1]
+def clock_sampler(index: int):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
+def algorithmic_bytes(tok: str, info, n: int, ncols: int | None = None) -> float:
+    """Bytes per SpMV launch per SURVEY.md §8(d) (device layout: fp64 values,
+    int32 column indices; x read once, y written once)."""
     fmt = tok.split("/")[0]
-    nnz, ncols = info["nnz"], n
+    nnz = info["nnz"]
+    ncols = n if ncols is None else ncols
+    ptrb = 8 if info.get("ptr64") else 4
     if fmt == "CSR":
-        return 12 * nnz + 4 * (n + 1) + 8 * ncols + 8 * n
+        return 12 * nnz + ptrb * (n + 1) + 8 * ncols + 8 * n
     if fmt == "DIA":
         return 8 * info["ndiag"] * n + 8 * ncols + 8 * n
     if fmt == "ELL":
@@ -273,57 +325,42 @@ def algorithmic_bytes(tag: str, info, n: int) -> float:
 
 
 def mgs_bytes(n: int, j: int, resident: bool = True) -> float:
-    """Algorithmic bytes of one Arnoldi orthogonalisation at column j.
-
-    Resident kernel (w kept on chip): read w once, each basis row V[0..j]
-    once, write the normalised w once -> 8n(j+3).  Streaming fallback: dot0
-    reads V0,w (16n); pass i reads w,V[i-1],V[i] and writes w (32n); final
-    reads w,V[j] and writes w (24n); normalise reads+writes w (16n)."""
+    """Algorithmic bytes of one Arnoldi orthogonalisation at column j: the
+    resident kernel reads w and V_0..V_j once and writes V_{j+1} once ->
+    8n(j+3); the streaming fallback re-reads w every pass."""
     if resident:
         return 8 * n * (j + 3)
     return 16 * n + 32 * n * j + 24 * n + 16 * n
 
 
-def config1_cg(P, device, _lib, models, start_cfg, reps: int = 3) -> dict:
-    """Side measurement (not `value`): BASELINE configs[0], CG fp64 on the 2-D
-    5-point Poisson 1024^2 (n = 1,048,576, nnz = 5,238,784), tol 1e-8,
-    b = A*1; async predict-while-solve from CSR/LibA/32 vs the fixed
-    default CSR-vector solve."""
-    import numpy as np
-    import torch
-    from paper_2411_10143_b200.solver import DeviceOptions
-    A = P.CsrMatrix.stencil((1024, 1024), [(0, 0), (0, -1), (0, 1), (-1, 0), (1, 0)],
-                            [4.0, -1.0, -1.0, -1.0, -1.0])
-    s = device.thread_stream()
-    ones = device.DeviceVector.from_numpy(np.ones(A.nrows), s)
-    b = device.DeviceVector(A.nrows)
-    _lib.check(_lib.lib().svb_spmv_sequential(A._device().handle, ones.ptr, b.ptr, s.handle))
-    s.sync()
-    params = P.GmresParams(tol=1e-8, max_iters=5000)
-    out = {"workload": "config1: CG fp64 Poisson 1024^2, tol 1e-8, b=A*1"}
-    with DeviceOptions(keep_solution_on_device=True):
-        P.async_solve(A, b, params, models, method="cg", initial_config=start_cfg)   # warm
-        ts, its, swaps = [], None, None
-        for _ in range(reps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = P.async_solve(A, b, params, models, method="cg", initial_config=start_cfg)
-            torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
-            its, swaps = r.iterations, [(x.iteration, x.config.token()) for x in r.config_timeline]
-        out.update({"async_s": statistics.median(ts), "iterations": its, "swaps": swaps,
-                    "converged": r.converged, "final_residual": r.final_residual})
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d = P.cg_solve(A, b, params, initial_config=start_cfg)
-        torch.cuda.synchronize()
-        out.update({"default_csr_vector_s": time.perf_counter() - t0, "default_iterations": d.iterations})
-    return out
+def info_of(mat) -> dict:
+    inf = mat._device().info
+    return {"nnz": int(inf.nnz), "ndiag": int(inf.ndiag), "width": int(inf.width),
+            "spill": int(inf.spill_nnz), "ptr64": bool(inf.ptr64)}
+
+
+def load_traffic(tag: str):
+    """ncu dram bytes per launch of `tag` (profiles/ncu_traffic.json, written
+    from one `ncu --set full` capture), or None."""
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        return json.loads(prof.read_text()).get(tag)
+    return None
 
 
 # ---------------------------------------------------------------------------
-# the B200 arm
+# the B200 arm: config 5, row-partitioned, every N
 # ---------------------------------------------------------------------------
+def stencil27():
+    offs, wts = [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                offs.append((dz, dy, dx))
+                wts.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
+    return offs, wts
+
+
 def b200_arm(args):
     ws, rank, local = dist_env()
     # SPMVTUNE_DIST_BACKEND=gloo: every rank on GPU 0, collectives staged
@@ -335,392 +372,395 @@ def b200_arm(args):
     os.environ.setdefault("SPMVTUNE_DEVICE", str(local))
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     import paper_2411_10143_b200 as P
     from paper_2411_10143_b200 import _lib, device
+    from paper_2411_10143_b200.distributed import (HostStagedComm, distributed_solve_slab,
+                                                    distributed_stencil_solve, stencil_block,
+                                                    stencil_partition)
     from paper_2411_10143_b200.solver import DeviceOptions
 
     torch.cuda.set_device(local)
-    if ws > 1 or args.workload == "config5":
-        import torch.distributed as dist
-        if not dist.is_initialized():
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29517")
-            if host_staged:
-                dist.init_process_group("gloo", rank=rank, world_size=ws)
-            else:
-                dist.init_process_group("nccl", rank=rank, world_size=ws,
-                                        device_id=torch.device("cuda", local))
-        return dist_arm(args, ws, rank, local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29517))
+        if host_staged:
+            dist.init_process_group("gloo", rank=rank, world_size=ws)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=torch.device("cuda", local))
+    comm_class = HostStagedComm if host_staged else None
     L = _lib.lib()
 
-    def barrier():
-        if ws > 1:
-            torch.distributed.barrier()
+    dims = (N3, N3, N3)
+    offs, wts = stencil27()
+    models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
+    params = P.GmresParams(tol=TOL, max_iters=20000)
+    bounds = stencil_partition(dims, ws)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    s = device.thread_stream(0)
+    ext = torch.cuda.ExternalStream(s.handle)
+    t0 = time.perf_counter()
+    blk = stencil_block(dims, offs, wts, r0, r1, s)          # this rank's slab, generated in HBM
+    gen_s = time.perf_counter() - t0
 
-    # --- inputs ------------------------------------------------------------
+    def step(timer=None):
+        t = {}
+        with DeviceOptions(timer=timer):
+            res, _ = distributed_stencil_solve("cg", dims, offs, wts, params, models=models, blk=blk,
+                                               comm_class=comm_class, timings=t)
+        return res, t
+
+    for _ in range(args.warmup):
+        step()
+
+    # --- timed region (slabs resident in HBM) -------------------------------
+    clocks = clock_sampler(local)
+    launches0 = _lib.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()        # no cyclic-GC pauses inside the timed steps
+    ev0.record(ext)
+    wall0 = time.perf_counter()
+    steps, results = [], []
+    for _ in range(args.steps):
+        res, t = step()
+        steps.append(t)
+        results.append({k: res[k] for k in ("converged", "iterations", "final", "config")})
+    ev1.record(ext)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    gc.enable()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    dev_s = ev0.elapsed_time(ev1) / 1e3
+    region = torch.tensor([max(dev_s, wall)], device="cpu" if host_staged else "cuda")
+    dist.all_reduce(region, op=dist.ReduceOp.MAX)
+    value = float(region.item()) / args.steps
+    its = results[-1]["iterations"]
+
+    # --- dominant kernel: events around every local SpMV of one instrumented
+    # solve on the solver stream (kept out of `value`: per-launch event
+    # records add host work)
+    timer = EventTimer()
+    res_i, t_i = step(timer)
+    kern = timer.summary()
+    cfg = P.SpmvConfig.from_token(results[-1]["config"])
+    tag = "spmv:" + cfg.token()
+    mat = blk._dev_csr if cfg.format is P.FormatTag.CSR else P.convert(blk._dev_csr, cfg.format)
+    inf = info_of(mat)
+    del mat
+    hbm, peak_kind = peaks()
+    ms = kern.get(tag, [])
+    spmv_bytes = algorithmic_bytes(cfg.token(), inf, blk.nloc, blk.window)
+    parts = 1 if (ws == 1) else max(1, round(len(ms) / max(1, res_i["iterations"] + 1)))
+    spmv_total_ms = sum(ms)
+    applies = len(ms) / parts
+    avg_ms = spmv_total_ms / max(1.0, applies)           # one local SpMV (all its row parts)
+    gbs = spmv_bytes / (avg_ms / 1e3) / 1e9 if ms else 0.0
+    roofline = {"kernel": tag + (" (k_dia)" if cfg.format is P.FormatTag.DIA else ""), "bound": "hbm",
+                "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                "traffic": load_traffic(f"config5:{tag}") if ws == 1 else None, "peak_kind": peak_kind,
+                "bytes_per_launch": spmv_bytes, "avg_launch_ms": avg_ms, "launches": len(ms),
+                "share_of_step": spmv_total_ms / 1e3 / max(1e-9, t_i["total_s"]),
+                "bytes_formula": "8*ndiag*n + 8*window + 8*n (DIA; SURVEY §8d)"}
+
+    # --- e2e: the same solve from this rank's pinned host slab ----------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_slab(args, blk, r0, r1, params, models, comm_class, ws)
+    gathered = [None] * ws
+    dist.all_gather_object(gathered, {"rank": rank, "rows": [r0, r1], "gen_s": gen_s,
+                                      "last_step": steps[-1], "spmv_ms": avg_ms, "gbs": gbs})
+    del blk
+    gc.collect()
+
+    cpu, detail = None, {}
+    if rank == 0 and ws == 1:
+        if not args.no_cpu:
+            try:
+                r = cpu_config5_sample(its)
+                cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+                cpu["extrapolated"] = True
+            except Exception as exc:  # measurement must not kill the bench line
+                cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                       "sample": f"failed: {exc}"[:300]}
+        if not args.no_extra:
+            for name, fn in (("config2_gmres_async", config2_detail), ("config1_cg", config1_detail),
+                             ("config3_cg_powerlaw", config3_detail)):
+                try:
+                    detail[name] = fn(args, P, device, _lib, models)
+                except Exception as exc:
+                    detail[name] = f"failed: {type(exc).__name__}: {exc}"[:400]
+    dist.barrier()
+    if rank == 0:
+        detail.update({"results": results[-1], "per_step": steps, "per_rank": gathered,
+                       "per_iteration_solve_s": steps[-1]["solve_s"] / max(1, its),
+                       "device_region_s": dev_s, "wall_region_s": wall,
+                       "slab_generation_s_rank0": gen_s})
+        line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload5(), "parallelism": f"row-partitioned x{ws}",
+                           "comm": "gloo, host-staged (path validation, not a performance number)"
+                           if host_staged else "nccl",
+                           "l2": "inputs larger than L2 (47 GB DIA + 71.5 GB CSR per GPU at N=1, 126 MB L2)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk, "detail": detail}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def e2e_slab(args, blk, r0, r1, params, models, comm_class, ws):
+    """Every rank copies its slab to pinned host memory once (outside the
+    clock), drops the device copy, then times solves through the public
+    per-rank entry point distributed_solve_slab: H2D of row_ptr/col_idx/
+    values/b + device validation + global features + cascade + conversion +
+    CG + D2H of x, all inside the clock."""
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_10143_b200 import _lib, device
+    from paper_2411_10143_b200.distributed import distributed_solve_slab
+    L = _lib.lib()
+    s = device.thread_stream(0)
+    csr = blk._dev_csr
+    n = blk.ncols_global
+    nloc, nnz = blk.nloc, (csr.nnz if csr is not None else 0)
+    handles = []
+
+    def pinned(count, dtype):
+        if count == 0:
+            return np.zeros(0, dtype)
+        h = ctypes.c_void_p()
+        nbytes = int(count) * np.dtype(dtype).itemsize
+        _lib.check(L.svb_host_alloc(nbytes, ctypes.byref(h)))
+        handles.append(h.value)
+        return np.frombuffer((ctypes.c_char * nbytes).from_address(h.value), dtype=dtype, count=int(count))
+
+    t0 = time.perf_counter()
+    hp, hc, hv, hb = pinned(nloc + 1, np.int64), pinned(nnz, np.int32), pinned(nnz, np.float64), \
+        pinned(nloc, np.float64)
+    if csr is not None:
+        _lib.check(L.svb_csr_export(csr._device().handle, blk.cmin, hp.ctypes.data, hc.ctypes.data,
+                                    hv.ctypes.data, s.handle))
+        # b = A*1 on this rank's rows, as the device-resident arm computes it
+        ones = device.DeviceVector(blk.window)
+        _lib.check(L.svb_fill(ones.ptr, blk.window, 1.0, s.handle))
+        bd = device.DeviceVector(nloc)
+        _lib.check(L.svb_spmv_sequential(csr._device().handle, ones.ptr, bd.ptr, s.handle))
+        device.copy(hb.ctypes.data, bd.ptr, bd.nbytes, s)
+        s.sync()
+        del ones, bd
+    else:
+        hp[:] = 0
+    prep_s = time.perf_counter() - t0
+    blk._dev_csr = None                      # the slab now lives on the host only
+    del csr
+    gc.collect()
+
+    def one():
+        t = {}
+        res = distributed_solve_slab("cg", r0, r1, n, hp, hc, hv, hb, params, models=models, timings=t,
+                                     comm_class=comm_class)
+        return res, t
+
+    one()                                     # warm (pool growth, first use of the slab path)
+    k = max(1, min(args.steps, args.e2e_steps))
+    dist.barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    phases = []
+    for _ in range(k):
+        res, t = one()
+        phases.append(t)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    dist.barrier()
+    dev = "cpu" if comm_class else "cuda"
+    tt = torch.tensor([wall], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    byts = torch.tensor([hp.nbytes + hc.nbytes + hv.nbytes + hb.nbytes, 8 * nloc], dtype=torch.float64,
+                        device=dev)
+    dist.all_reduce(byts)
+    del hp, hc, hv, hb
+    for h in handles:
+        L.svb_host_free(h)
+    return {"value": float(tt.item()) / k, "unit": "s", "h2d_bytes_per_step": int(byts[0].item()),
+            "d2h_bytes_per_step": int(byts[1].item()), "steps": k, "iterations": res["iterations"],
+            "converged": res["converged"], "final_residual": res["final"], "phases_last": phases[-1],
+            "host_slab_prep_s": prep_s,
+            "note": "each rank: pinned host slab (row_ptr int64, GLOBAL col_idx int32, values f64, b f64) -> "
+                    "distributed_solve_slab (H2D + device validation + features + cascade + conversion + "
+                    "CG) -> x slice to host; max over ranks; totals over ranks"}
+
+
+# ---------------------------------------------------------------------------
+# single-GPU detail workloads (N = 1, rank 0)
+# ---------------------------------------------------------------------------
+def _timed(fn, reps=3):
+    import torch
+    ts, rep = [], None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        if hasattr(rep, "solution"):
+            rep.solution = None
+    return statistics.median(ts), rep
+
+
+def config2_detail(args, P, device, _lib, models) -> dict:
+    """BASELINE configs[1]: GMRES(30) async predict-while-solve (the paper's
+    AsyGMRES) on one B200, device-resident and end to end from pinned host
+    CSR, against the default CSR-vector solve and predict-then-solve, with
+    the Arnoldi kernel's roofline from per-launch events."""
+    import numpy as np
+    import torch
+    from paper_2411_10143_b200.solver import DeviceOptions
     offs, wts = [], []
     for dy in (-1, 0, 1):
         for dx in (-1, 0, 1):
             offs.append((dy, dx))
             wts.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
-    A = P.CsrMatrix.stencil((NX, NX), offs, wts)              # generated in HBM
+    A = P.CsrMatrix.stencil((NX2, NX2), offs, wts)
     n = A.nrows
-    models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
     params = P.GmresParams(restart_m=RESTART, tol=TOL, max_iters=1000)
-    start_cfg = P.GPU_DEFAULT_CONFIG
+    start = P.GPU_DEFAULT_CONFIG
     s = device.thread_stream()
     ones = device.DeviceVector.from_numpy(np.ones(n), s)
     b_dev = device.DeviceVector(n)
-    _lib.check(L.svb_spmv_sequential(A._device().handle, ones.ptr, b_dev.ptr, s.handle))  # b = A*1
+    _lib.check(_lib.lib().svb_spmv_sequential(A._device().handle, ones.ptr, b_dev.ptr, s.handle))
     s.sync()
-
-    def step(timer=None):
+    out = {"workload": WORKLOAD2, "metric": METRIC2}
+    with DeviceOptions(keep_solution_on_device=True):
+        for _ in range(3):
+            P.async_solve(A, b_dev, params, models, initial_config=start).solution = None
+        reps = max(5, min(args.steps, 20))
+        ts, swaps = [], []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = P.async_solve(A, b_dev, params, models, initial_config=start)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+            swaps.append([(x.iteration, x.config.token()) for x in r.config_timeline])
+            r.solution = None
+        out.update({"async_s": statistics.median(ts), "async_runs_s": ts, "iterations": r.iterations,
+                    "converged": r.converged, "final_residual": r.final_residual, "swaps": swaps[-1]})
+        out["default_csr_vector_s"], d = _timed(lambda: P.gmres_solve(A, b_dev, params, initial_config=start))
+        out["default_iterations"] = d.iterations
+        out["sequential_s"], sq = _timed(lambda: P.sequential_predict_solve(A, b_dev, params, models))
+        out["sequential_phases"] = sq.phases
+        timer = EventTimer()
         with DeviceOptions(timer=timer, keep_solution_on_device=True):
-            return P.async_solve(A, b_dev, params, models, initial_config=start_cfg)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    # --- timed region (device-resident inputs) -----------------------------
-    try:
-        clocks = NvmlClockSampler(local)
-    except Exception:
-        clocks = ClockSampler(local)
-    launches0 = _lib.launch_count()
-    barrier()
-    torch.cuda.synchronize()
-    t_ev0 = torch.cuda.Event(enable_timing=True)
-    t_ev1 = torch.cuda.Event(enable_timing=True)
-    per_step, reports = [], []
-    gc.collect()
-    gc.disable()      # no cyclic-GC pauses inside the timed steps
-    t_ev0.record()
-    wall0 = time.perf_counter()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        rep = step()
-        per_step.append(time.perf_counter() - t0)
-        rep.solution = None     # free the device solution now: no pool growth across steps
-        reports.append(rep)
-    torch.cuda.synchronize()
-    t_ev1.record()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    gc.enable()
-    barrier()
-    launches = _lib.launch_count() - launches0
-    clk = clocks.stop()
-    dev_ms = t_ev0.elapsed_time(t_ev1)
-    # whole-region device time (events on the default stream bracket all work,
-    # the solve's own streams are synchronised inside each step)
-    total_s = max(dev_ms / 1e3, wall)
-    if ws > 1:
-        t = torch.tensor([total_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_s = float(t.item())
-    value = total_s / args.steps
-
-    # --- kernel timing: separate instrumented steps (CUDA events around every
-    # SpMV and Arnoldi launch on the solver stream); kept out of `value`
-    # because recording events per launch adds host work to the step
-    timer = EventTimer()
-    timer.active = True
-    prof_steps = max(1, min(args.steps, 3))
-    prof_reports = []
-    for _ in range(prof_steps):
-        r = step(timer)
-        r.solution = None
-        prof_reports.append(r)
-    kern = timer.summary()
-
-    # --- per-kernel roofline ----------------------------------------------------
-    hbm, peak_kind = peaks()
-    infos = {}
-    last = reports[-1]
-    for swap in last.config_timeline:
-        tok = swap.config.token()
-        rep = A if swap.config.format is P.FormatTag.CSR else P.convert(A, swap.config.format)
-        inf = rep._device().info
-        infos[tok] = {"nnz": int(inf.nnz), "ndiag": int(inf.ndiag), "width": int(inf.width),
-                      "spill": int(inf.spill_nnz)}
+            ri = P.async_solve(A, b_dev, params, models, initial_config=start)
+        kern = timer.summary()
+    hbm, _ = peaks()
     groups = {}
     for tag, ms in kern.items():
         tot = sum(ms)
         if tag.startswith("spmv:"):
             tok = tag.split(":", 1)[1]
-            if tok not in infos:
-                continue
-            byts = algorithmic_bytes(tag, infos[tok], n) * len(ms)
+            mat = A if tok.startswith("CSR") else P.convert(A, P.SpmvConfig.from_token(tok).format)
+            byts = algorithmic_bytes(tok, info_of(mat), n) * len(ms)
         elif tag == "mgs":
-            # j cycles 0..restart-1 across steps; the column of each call is
-            # reconstructed from the iteration schedule of the reports
-            js = []
-            for r in prof_reports:
-                js += [it % RESTART for it in range(r.iterations)]
-            resident = os.environ.get("SPMVTUNE_MGS") != "stream"
-            byts = sum(mgs_bytes(n, j, resident) for j in js[:len(ms)])
+            js = [it % RESTART for it in range(ri.iterations)]
+            byts = sum(mgs_bytes(n, j) for j in js[:len(ms)])
         else:
             continue
-        groups[tag] = {"launches": len(ms), "ms_total": tot, "ms_avg": tot / len(ms),
-                       "gbs": byts / (tot / 1e3) / 1e9, "bytes_per_launch": byts / len(ms)}
-    step_ms = value * 1e3
-    for g in groups.values():
-        g["share_of_step"] = g["ms_total"] / prof_steps / step_ms
-    dom_tag = max(groups, key=lambda t: groups[t]["ms_total"]) if groups else None
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists() and dom_tag:
-        tr = json.loads(prof.read_text())
-        traffic = tr.get(dom_tag)
-    roofline = None
-    if dom_tag:
-        g = groups[dom_tag]
-        roofline = {"kernel": dom_tag, "bound": "hbm", "achieved": round(g["gbs"], 1),
-                    "peak": hbm, "unit": "GB/s", "frac": round(g["gbs"] / hbm, 4),
-                    "traffic": traffic, "peak_kind": peak_kind,
-                    "bytes_per_launch": g["bytes_per_launch"], "avg_launch_ms": g["ms_avg"]}
+        groups[tag] = {"launches": len(ms), "ms_avg": tot / len(ms), "gbs": byts / (tot / 1e3) / 1e9,
+                       "frac": byts / (tot / 1e3) / 1e9 / hbm, "share_of_solve": tot / 1e3 / out["async_s"]}
+    out["kernels"] = groups
+    # e2e from pinned host CSR (int64 indices, the reference layout)
+    rp, ci, vv = np.asarray(A.row_ptr), np.asarray(A.col_idx), np.asarray(A.values)
+    bh = b_dev.to_numpy(s)
+    pin = {}
+    for k, arr in (("rp", rp), ("ci", ci), ("vv", vv), ("b", bh)):
+        t = torch.empty(arr.size, dtype=torch.from_numpy(arr[:1].copy()).dtype, pin_memory=True)
+        t.numpy()[:] = arr
+        pin[k] = t
+    Ah = P.CsrMatrix(n, n, pin["rp"].numpy(), pin["ci"].numpy(), pin["vv"].numpy())
+    b_host = pin["b"].numpy()
 
-    # --- end-to-end through the public API from pinned host buffers -----------------
-    e2e = None
-    if rank == 0 or ws > 1:
-        rp = np.asarray(A.row_ptr)
-        ci = np.asarray(A.col_idx)
-        vv = np.asarray(A.values)
-        bh = b_dev.to_numpy(s)
-        pin = {}
-        for k, arr in (("rp", rp), ("ci", ci), ("vv", vv), ("b", bh)):
-            t = torch.empty(arr.size, dtype=torch.from_numpy(arr[:1]).dtype, pin_memory=True)
-            t.numpy()[:] = arr
-            pin[k] = t
-        Ah = P.CsrMatrix(n, n, pin["rp"].numpy(), pin["ci"].numpy(), pin["vv"].numpy())
-        b_host = pin["b"].numpy()
-
-        def e2e_step():
-            Ah._dev = None                     # drop the device copy: upload inside the clock
-            rep = P.async_solve(Ah, b_host, params, models, initial_config=start_cfg)
-            return rep
-        e2e_step()
-        torch.cuda.synchronize()
-        k_e2e = max(1, min(args.steps, 5))
-        t0 = time.perf_counter()
-        for _ in range(k_e2e):
-            rep_e = e2e_step()
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / k_e2e
-        h2d = rp.nbytes + ci.nbytes + vv.nbytes + bh.nbytes
-        d2h = rep_e.solution.nbytes + 48 * (rep_e.iterations + 4)
-        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
-               "note": "CsrMatrix from pinned host int64/f64 arrays (upload + narrowing inside "
-                       "the clock) -> async_solve -> solution to host"}
-
-    # --- comparison solves (not timed as `value`) ---------------------------
-    detail = {}
-    if rank == 0:
-        with DeviceOptions(keep_solution_on_device=True):
-            def timed(fn, reps=3):          # median of `reps` warm runs
-                ts, rep = [], None
-                for _ in range(reps):
-                    torch.cuda.synchronize()
-                    t0 = time.perf_counter()
-                    rep = fn()
-                    torch.cuda.synchronize()
-                    ts.append(time.perf_counter() - t0)
-                    rep.solution = None
-                return statistics.median(ts), rep
-            dt, d = timed(lambda: P.gmres_solve(A, b_dev, params, initial_config=start_cfg))
-            detail["default_csr_vector_gpu_s"] = dt
-            detail["default_iterations"] = d.iterations
-            st, sq = timed(lambda: P.sequential_predict_solve(A, b_dev, params, models))
-            detail["sequential_gpu_s"] = st
-            detail["sequential_phases"] = sq.phases
-        if not args.no_extra:
-            detail["config1_cg"] = config1_cg(P, device, _lib, models, start_cfg)
-    detail.update({
-        "iterations": last.iterations, "converged": last.converged,
-        "final_residual": last.final_residual,
-        "timeline": [sw.to_dict() for sw in last.config_timeline],
-        "advisor_outcome": last.advisor_outcome, "per_step_wall_s": per_step,
-        "per_step_swaps": [[(sw.iteration, sw.config.token(), round(sw.swap_cost_seconds, 5))
-                            for sw in r.config_timeline] for r in reports],
-        "device_region_ms": dev_ms, "wall_region_s": wall, "kernels": groups})
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        try:
-            r = run_cpu_sample(1, 0, last.iterations)
-            cpu = {"value": r["value"], "unit": "s", "cores": r["cores"], "kind": r["kind"],
-                   "sample": r["sample"], "phases": r["phases"], "cpu_model": r.get("cpu_model")}
-        except Exception as exc:  # measurement must not kill the bench line
-            cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"failed: {exc}"[:300]}
-
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-                # one fixed system at every N (N > 1: row-partitioned, dist_arm)
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "mode": "async",
-                           "parallelism": f"replicas{ws}" if ws > 1 else "single",
-                           "l2": "inputs larger than L2 (CSR 448 MB + Krylov basis 992 MB vs 126 MB L2)"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(launches), "clocks": clk, "detail": detail}
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
-
-
-# ---------------------------------------------------------------------------
-# row-partitioned arm (torchrun, N > 1; or --workload config5 at any N)
-# ---------------------------------------------------------------------------
-def stencil_problem(workload: str):
-    if workload == "config5":
-        offs, wts = [], []
-        for dz in (-1, 0, 1):
-            for dy in (-1, 0, 1):
-                for dx in (-1, 0, 1):
-                    offs.append((dz, dy, dx))
-                    wts.append(26.0 if (dx, dy, dz) == (0, 0, 0) else -1.0)
-        n3 = int(os.environ.get("SPMVTUNE_CONFIG5_N", "600"))
-        return ("cg", (n3, n3, n3), offs, wts,
-                f"config5: CG fp64, tol {TOL:g}, b=A*1, 3-D 27-point Laplacian {n3}^3 "
-                f"(n={n3 ** 3:,}, nnz={(3 * n3 - 2) ** 3:,}), row-partitioned z-slabs generated "
-                "per rank on the device, cascade on exact global features, NCCL halo + all-reduce")
-    offs, wts = [], []
-    for dy in (-1, 0, 1):
-        for dx in (-1, 0, 1):
-            offs.append((dy, dx))
-            wts.append(8.5 if (dx, dy) == (0, 0) else -1.0 - 0.25 * (dx + dy))
-    return ("gmres", (NX, NX), offs, wts, WORKLOAD.replace("async predict-while-solve starting on "
-            "CSR/LibA/32", "row-partitioned predict-then-solve (cascade on exact global features, "
-            "NCCL halo + all-reduce)"))
-
-
-def dist_arm(args, ws, rank, local):
-    """Time-to-solution of the row-partitioned solve (distributed.py): each
-    rank generates its slab on its GPU (outside the clock, like the single-GPU
-    arm's matrix), then every step runs global features -> cascade ->
-    conversion -> solve.  Strong scaling: the problem is fixed as N grows."""
-    import torch
-    import torch.distributed as dist
-
-    import paper_2411_10143_b200 as P
-    from paper_2411_10143_b200 import _lib, device
-    from paper_2411_10143_b200.distributed import HostStagedComm, distributed_stencil_solve, \
-        stencil_block, stencil_partition
-
-    comm_class = HostStagedComm if os.environ.get("SPMVTUNE_DIST_BACKEND") == "gloo" else None
-
-    method, dims, offs, wts, workload = stencil_problem(args.workload)
-    models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
-    params = P.GmresParams(restart_m=RESTART, tol=TOL, max_iters=20000)
-    bounds = stencil_partition(dims, ws)
-    s = device.thread_stream(0)
+    def e2e_step():
+        Ah._dev = None                      # drop the device copy: upload inside the clock
+        return P.async_solve(Ah, b_host, params, models, initial_config=start)
+    e2e_step()
+    k = max(5, min(args.steps, 20))
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    blk = stencil_block(dims, offs, wts, int(bounds[rank]), int(bounds[rank + 1]), s)
+    for _ in range(k):
+        re = e2e_step()
+    torch.cuda.synchronize()
+    out["e2e"] = {"value": (time.perf_counter() - t0) / k, "unit": "s", "steps": k,
+                  "h2d_bytes_per_step": int(rp.nbytes + ci.nbytes + vv.nbytes + bh.nbytes),
+                  "d2h_bytes_per_step": int(re.solution.nbytes + 48 * (re.iterations + 4)),
+                  "note": "CsrMatrix from pinned host int64/f64 arrays -> async_solve -> solution to host"}
+    return out
+
+
+def config1_detail(args, P, device, _lib, models) -> dict:
+    """BASELINE configs[0]: CG fp64 on the 2-D 5-point Poisson 1024^2
+    (n = 1,048,576, nnz = 5,238,784), tol 1e-8, b = A*1; async
+    predict-while-solve from CSR/LibA/32 vs the fixed default CSR-vector solve."""
+    import numpy as np
+    from paper_2411_10143_b200.solver import DeviceOptions
+    A = P.CsrMatrix.stencil((1024, 1024), [(0, 0), (0, -1), (0, 1), (-1, 0), (1, 0)],
+                            [4.0, -1.0, -1.0, -1.0, -1.0])
+    s = device.thread_stream()
+    ones = device.DeviceVector.from_numpy(np.ones(A.nrows), s)
+    b = device.DeviceVector(A.nrows)
+    _lib.check(_lib.lib().svb_spmv_sequential(A._device().handle, ones.ptr, b.ptr, s.handle))
+    s.sync()
+    params = P.GmresParams(tol=TOL, max_iters=5000)
+    start = P.GPU_DEFAULT_CONFIG
+    out = {"workload": "config1: CG fp64 Poisson 1024^2, tol 1e-8, b=A*1"}
+    with DeviceOptions(keep_solution_on_device=True):
+        P.async_solve(A, b, params, models, method="cg", initial_config=start).solution = None
+        out["async_s"], r = _timed(lambda: P.async_solve(A, b, params, models, method="cg",
+                                                         initial_config=start), reps=5)
+        out.update({"iterations": r.iterations, "converged": r.converged, "final_residual": r.final_residual,
+                    "swaps": [(x.iteration, x.config.token()) for x in r.config_timeline]})
+        out["default_csr_vector_s"], d = _timed(lambda: P.cg_solve(A, b, params, initial_config=start), reps=3)
+        out["default_iterations"] = d.iterations
+    return out
+
+
+def config3_detail(args, P, device, _lib, models) -> dict:
+    """BASELINE configs[2]: CG on the power-law SPD matrix (8 M rows, ~112 M
+    nnz; device-built, bit-identical to generators.powerlaw_spd), b random
+    seed 0 (solver.py:190-191), tol 1e-8: async from CSR/LibA/32 with the
+    shipped and the B200-trained cascade, vs the default CSR-vector solve."""
+    from paper_2411_10143_b200 import generators as G
+    from paper_2411_10143_b200.solver import DeviceOptions, default_rhs
+    t0 = time.perf_counter()
+    A = G.powerlaw_spd_device(8_000_000, seed=0)
     gen_s = time.perf_counter() - t0
-
-    def step():
-        t = {}
-        res, _ = distributed_stencil_solve(method, dims, offs, wts, params, models=models, blk=blk,
-                                           comm_class=comm_class,
-                                           timings=t)
-        return res, t
-
-    for _ in range(args.warmup):
-        step()
-    try:
-        clocks = NvmlClockSampler(local)
-    except Exception:
-        clocks = ClockSampler(local)
-    launches0 = _lib.launch_count()
-    dist.barrier()
-    torch.cuda.synchronize()
-    steps, results = [], []
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        res, t = step()
-        steps.append(t)
-        results.append({k: res[k] for k in ("converged", "iterations", "final", "config")})
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t_all
-    dist.barrier()
-    clk = clocks.stop()
-    launches = _lib.launch_count() - launches0
-    tt = torch.tensor([wall], device="cpu" if comm_class else "cuda")
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    value = float(tt.item()) / args.steps
-
-    # roofline: the local SpMV in the predicted configuration, events on our stream
-    cfg = P.SpmvConfig.from_token(results[-1]["config"])
-    csr = blk._dev_csr
-    mat = csr if cfg.format is P.FormatTag.CSR else P.convert(csr, cfg.format)
-    inf = mat._device().info
-    xw = device.DeviceVector(blk.window)
-    _lib.check(_lib.lib().svb_fill(xw.ptr, blk.window, 1.0, s.handle))
-    yl = device.DeviceVector(blk.nloc)
-    ext = torch.cuda.ExternalStream(s.handle)
-    from paper_2411_10143_b200.kernels import default_workers, launch
-    for _ in range(3):
-        launch(cfg, mat, xw.ptr, yl.ptr, workers=default_workers(), stream=s)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
-    e0.record(ext)
-    for _ in range(reps):
-        launch(cfg, mat, xw.ptr, yl.ptr, workers=default_workers(), stream=s)
-    e1.record(ext)
-    torch.cuda.synchronize()
-    spmv_ms = e0.elapsed_time(e1) / reps
-    n_loc = blk.nloc
-    info = {"nnz": int(inf.nnz), "ndiag": int(inf.ndiag), "width": int(inf.width),
-            "spill": int(inf.spill_nnz)}
-    byts = algorithmic_bytes("spmv:" + cfg.token(), info, n_loc)
-    byts += 8 * (blk.window - n_loc)          # x is the window, not just the local rows
-    hbm, peak_kind = peaks()
-    gbs = byts / (spmv_ms / 1e3) / 1e9
-    roofline = {"kernel": "spmv:" + cfg.token(), "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(gbs / hbm, 4), "traffic": None, "peak_kind": peak_kind,
-                "bytes_per_launch": byts, "avg_launch_ms": spmv_ms}
-    its = results[-1]["iterations"]
-    per_iter = {k: v / max(1, its) for k, v in steps[-1].items() if k == "solve_s"}
-    gathered = [None] * ws
-    dist.all_gather_object(gathered, {"rank": rank, "rows": [int(bounds[rank]), int(bounds[rank + 1])],
-                                      "spmv_ms": spmv_ms, "gbs": gbs, "gen_s": gen_s,
-                                      "last_step": steps[-1]})
-    cpu = None
-    if rank == 0 and ws == 1 and args.workload == "config5" and not args.no_cpu:
-        try:
-            env = dict(os.environ)
-            env["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
-            env.pop("CUDA_VISIBLE_DEVICES", None)
-            cmd = [sys.executable, "-m", "oracle.bench_cpu", "--laplace27", "120", "--iters", "4",
-                   "--total-iters", str(results[-1]["iterations"]), "--target", str(dims[0])]
-            o = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
-            r = json.loads(o.stdout.strip().splitlines()[-1])
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
-        except Exception as exc:  # measurement must not kill the bench line
-            cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"failed: {exc}"[:300]}
-    if rank == 0:
-        line = {"metric": METRIC5 if args.workload == "config5" else METRIC,
-                "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "parallelism": f"row-partitioned x{ws}",
-                           "comm": "gloo, host-staged (path validation, not a performance number)"
-                           if comm_class else "nccl",
-                           "l2": "inputs larger than L2"},
-                "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": None, "gpu_launches": int(launches), "clocks": clk,
-                "detail": {"results": results[-1], "per_step": steps, "per_rank": gathered,
-                           "per_iteration_solve_s": per_iter,
-                           "cpu_baseline_note": "the reference arm's CPU path cannot hold this "
-                           "matrix (int64 CSR >= 140 GB) — see BASELINE configs[4]"
-                           if args.workload == "config5" else "single-GPU line carries it"}}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+    params = P.GmresParams(tol=TOL, max_iters=20000, rhs="random", seed=0)
+    start = P.GPU_DEFAULT_CONFIG
+    b = default_rhs(A, params)
+    out = {"workload": f"config3: CG fp64 power-law SPD n={A.nrows:,} nnz={A.nnz:,}, b random seed 0",
+           "generation_s": gen_s}
+    b200 = P.CascadeModelSet.load_dir(P.B200_MODELS_DIR)
+    with DeviceOptions(keep_solution_on_device=True):
+        for name, ms in (("shipped", models), ("b200", b200)):
+            P.async_solve(A, b, params, ms, method="cg", initial_config=start).solution = None
+            t, r = _timed(lambda: P.async_solve(A, b, params, ms, method="cg", initial_config=start))
+            out[f"async_{name}_models_s"] = t
+            out[f"async_{name}_models"] = {"iterations": r.iterations, "converged": r.converged,
+                                           "swaps": [(x.iteration, x.config.token()) for x in r.config_timeline]}
+        out["default_csr_vector_s"], d = _timed(lambda: P.cg_solve(A, b, params, initial_config=start))
+        out["default_iterations"] = d.iterations
+    return out
 
 
 def main(argv=None):
@@ -729,21 +769,26 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--total-iters", type=int, default=77,
-                    help="reference arm: GMRES iterations the solve takes (77 at config 2)")
+    ap.add_argument("--total-iters", type=int, default=763,
+                    help="reference arm: CG iterations the 600^3 solve takes (763, measured on B200)")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="timed e2e solves (each re-uploads the slab)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-extra", action="store_true", help="skip the config-1 CG side measurement")
-    ap.add_argument("--workload", default="config2", choices=["config2", "config5"],
-                    help="config5 = row-partitioned CG on the 27-point Laplacian 600^3 (any N); "
-                         "N > 1 always runs the row-partitioned solver")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 1/2/3 detail workloads")
     args = ap.parse_args(argv)
-    if args.warmup < 0 or args.steps < 1:
-        raise SystemExit("--steps >= 1 and --warmup >= 0")
+    if args.warmup < 0 or args.steps < 1 or args.gpus < 1:
+        raise SystemExit("--steps >= 1, --warmup >= 0, --gpus >= 1")
     if args.impl == "reference":
         reference_arm(args)
-    else:
-        b200_arm(args)
+        return 0
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return self_launch(args)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws_env}: launch one rank per GPU")
+    b200_arm(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -133,6 +133,23 @@ int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
  * whose interior SpMV overlaps the halo exchange. */
 int svb_csr_row_slice(const svb_matrix* src, int64_t r0, int64_t r1, void* stream,
                       svb_matrix** out);
+/* A row-partitioned rank's own host slab (distributed_solve_slab, the
+ * per-rank form of distributed_solve's CsrMatrix input, formats.py:103-146):
+ * rows [r0, r0 + nrows) of a matrix with ncols_global columns; row_ptr is
+ * slab-local (row_ptr[0] = 0, row_ptr[nrows] = nnz); col_idx holds GLOBAL
+ * column indices, int64 (the reference's dtype) when cols_i64 != 0, else
+ * int32.  Uploaded and validated on the device with the CsrMatrix rules
+ * and messages (endpoints, non-decreasing row_ptr, column range, strictly
+ * increasing columns -> SVB_DIM_MISMATCH); stored with columns relative to
+ * the rank's window [cmin, cmax] (hull of the columns and the own rows),
+ * returned in window[2]. */
+int svb_csr_create_slab(int64_t nrows, int64_t ncols_global, int64_t nnz, int64_t r0,
+                        const int64_t* row_ptr_host, const void* col_idx_host, int32_t cols_i64,
+                        const double* vals_host, void* stream, int64_t* window, svb_matrix** out);
+/* CSR handle -> caller-owned host slab: row_ptr int64[nrows+1], columns
+ * int32[nnz] plus col_shift (window-relative -> global), values f64[nnz]. */
+int svb_csr_export(const svb_matrix* m, int64_t col_shift, int64_t* row_ptr_host, int32_t* cols_host,
+                   double* vals_host, void* stream);
 /* EllMatrix(nrows, ncols, width, col_idx, values): column-major (nrows x width)
  * arrays, i.e. cell (i, k) at k*nrows + i; sentinel column = ncols. */
 int svb_ell_create(int64_t nrows, int64_t ncols, int64_t width, const int64_t* cols_host,
@@ -208,6 +225,12 @@ int svb_spmv_sequential(const svb_matrix* csr, const double* x_dev, double* y_de
  * ndiag}; the host evaluates the 15 float features with the reference's own
  * expressions (features.py:103-110, 147-150), making them bit-exact. */
 int svb_features(const svb_matrix* csr, int64_t* agg_host, void* stream);
+/* The distinct diagonal offsets (col - row) of a CSR handle plus `shift`,
+ * ascending (the ndiag feature's set, features.py:118-126; a row-partitioned
+ * rank passes shift = cmin - r0 for global offsets so the ranks' sets can be
+ * united exactly).  *count = number of offsets; min(count, cap) are copied. */
+int svb_diag_offsets(const svb_matrix* csr, int64_t shift, int64_t* out_host, int64_t cap, int64_t* count,
+                     void* stream);
 
 /* ---- Krylov workspaces (solver.py:219-342; CG is new) ---- */
 typedef struct svb_krylov svb_krylov;
@@ -222,8 +245,10 @@ typedef struct {
   int64_t count;     /* batched CG: iterations executed since svb_cg_batch_reset */
 } svb_krylov_status;
 
-/* n rows, restart m (GMRES; m = 0 for CG).  Owns V[(m+1) x n], H, Givens
- * state, CG vectors and the mapped status block. */
+/* n rows, restart m (GMRES, 1 <= m <= 24000; m = 0 for CG).  Owns
+ * V[(m+1) x n], H, Givens state, CG vectors and the mapped status block.
+ * SVB_INVALID above 24000 (y of the x update is staged in shared memory);
+ * SVB_OOM when V does not fit the device. */
 int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out);
 int svb_krylov_destroy(svb_krylov* k);
 /* device pointers of workspace vectors: 0..m = V rows; -1 = x; -2 = b;

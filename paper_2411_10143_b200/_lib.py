@@ -109,6 +109,9 @@ _SIGS = {
     "svb_graph_launch": [_P, _P],
     "svb_graph_destroy": [_P],
     "svb_csr_row_slice": [_P, C.c_int64, C.c_int64, _P, _PP],
+    "svb_csr_create_slab": [_I64, _I64, _I64, _I64, _P, _P, _I32, _P, _P, _PI64, _PP],
+    "svb_csr_export": [_P, _I64, _P, _P, _P, _P],
+    "svb_diag_offsets": [_P, _I64, _PI64, _I64, _PI64, _P],
     "svb_mailbox_create": [_PP],
     "svb_mailbox_destroy": [_P],
     "svb_mailbox_publish": [_P, _P, SvbConfig, _P, C.c_double],
@@ -184,6 +187,14 @@ def load():
     return _lib
 
 
+def device_index() -> int:
+    """The CUDA device this process's library calls run on (SPMVTUNE_DEVICE,
+    else LOCAL_RANK, else 0)."""
+    if os.environ.get("SPMVTUNE_DEVICE") is not None:
+        return int(os.environ["SPMVTUNE_DEVICE"])
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def lib():
     """The library, with the CUDA device selected for the calling process."""
     global _initialised
@@ -191,9 +202,7 @@ def lib():
     if not _initialised:
         with _lock:
             if not _initialised:
-                dev = int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("SPMVTUNE_DEVICE") is None \
-                    else int(os.environ["SPMVTUNE_DEVICE"])
-                check(L.svb_init(dev))
+                check(L.svb_init(device_index()))
                 _initialised = True
     return L
 

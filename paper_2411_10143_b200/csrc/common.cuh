@@ -11,6 +11,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <string>
 
@@ -70,6 +71,18 @@ int guard(F&& body) {
     set_error(e.what());
     return SVB_INVALID;
   }
+}
+
+// Row pointers are int32 on the device unless nnz >= 2^31 (config 5 on one
+// GPU).  SPMVTUNE_FORCE_PTR64=1 makes every new CSR/COO handle use int64 row
+// pointers regardless of size: the test hook that runs the int64 kernels on
+// small matrices the CPU oracle can check.
+inline bool want_ptr64(int64_t nnz) {
+  static const bool forced = [] {
+    const char* e = std::getenv("SPMVTUNE_FORCE_PTR64");
+    return e && e[0] == '1';
+  }();
+  return forced || nnz >= INT32_MAX;
 }
 
 // ---------------------------------------------------------------------------

@@ -378,7 +378,7 @@ static svb_matrix* new_like(const RowView& v, int fmt) {
 
 static svb_matrix* build_csr(const RowView& v, cudaStream_t s) {
   auto m = new_like(v, SVB_CSR);
-  m->ptr64 = v.nnz >= INT32_MAX;
+  m->ptr64 = want_ptr64(v.nnz);
   if (m->ptr64) m->ptr = v.ptr;
   else {
     m->ptr = alloc((v.nrows + 1) * 4, s);
@@ -391,7 +391,7 @@ static svb_matrix* build_csr(const RowView& v, cudaStream_t s) {
 
 static svb_matrix* build_coo(const RowView& v, const svb_matrix* src, cudaStream_t s) {
   auto m = new_like(v, SVB_COO);
-  m->ptr64 = v.nnz >= INT32_MAX;
+  m->ptr64 = want_ptr64(v.nnz);
   if (v.rows) m->rows = v.rows;
   else {
     svb_matrix tmp;  // CSR-shaped view over the row pointer for the expansion kernel

@@ -8,6 +8,8 @@
 // makes the aggregates independent of the reduction order, and the host
 // evaluates the floats with the reference's own expressions, so the feature
 // vector is bit-identical to the CPU path.
+#include <algorithm>
+
 #include "matrix.cuh"
 
 namespace svb {
@@ -170,6 +172,24 @@ __global__ void k_popcount(int64_t nwords, const unsigned* __restrict__ bits,
   }
 }
 
+// set bits of the diagonal bitmap -> offsets (bit - (nrows - 1) + shift),
+// unordered (the host sorts them)
+__global__ void k_bits_to_offsets(int64_t nwords, const unsigned* __restrict__ bits, int64_t base,
+                                  long long* __restrict__ out, int64_t cap, unsigned long long* __restrict__ cnt) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    unsigned b = bits[w];
+    if (!b) continue;
+    unsigned long long at = atomicAdd(cnt, (unsigned long long)__popc(b));
+    while (b) {
+      const int k = __ffs(b) - 1;
+      b &= b - 1;
+      if ((int64_t)at < cap) out[at] = (long long)(w * 32 + k) + base;
+      ++at;
+    }
+  }
+}
+
 }  // namespace svb
 
 using namespace svb;
@@ -217,5 +237,43 @@ extern "C" int svb_features(const svb_matrix* m, int64_t* agg, void* stream) {
     agg[4] = (int64_t)h.a.span;
     agg[5] = (int64_t)h.a.runs;
     agg[6] = (int64_t)h.ndiag;
+  });
+}
+
+extern "C" int svb_diag_offsets(const svb_matrix* m, int64_t shift, int64_t* out_host, int64_t cap, int64_t* count,
+                                void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(m && count && (cap == 0 || out_host), SVB_INVALID, "null argument");
+    SVB_REQUIRE(m->fmt == SVB_CSR, SVB_UNSUPPORTED_CONFIG, "diagonal offsets need a CSR matrix");
+    Buf bits;
+    {
+      std::lock_guard<std::mutex> lk(m->mu);
+      bits = m->diag_bits;
+    }
+    if (!bits) {   // the feature pass builds (and caches) the bitmap
+      int64_t agg[7];
+      const int st = svb_features(m, agg, stream);
+      if (st != SVB_OK) throw Error{st, get_error()};
+      std::lock_guard<std::mutex> lk(m->mu);
+      bits = m->diag_bits;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nwords = (m->nrows + m->ncols - 1 + 31) / 32;
+    Buf tmp = alloc(8 + std::max<int64_t>(cap, 1) * 8, s);
+    auto* cnt = ptr<unsigned long long>(tmp);
+    SVB_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, s));
+    k_bits_to_offsets<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(bits), shift - (m->nrows - 1),
+                                                              ptr<long long>(tmp) + 1, cap, cnt);
+    SVB_CHECK_LAUNCH();
+    unsigned long long c = 0;
+    SVB_CUDA_TRY(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    *count = (int64_t)c;
+    const int64_t k = std::min<int64_t>((int64_t)c, cap);
+    if (k > 0) {
+      SVB_CUDA_TRY(cudaMemcpyAsync(out_host, ptr<long long>(tmp) + 1, k * 8, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+      std::sort(out_host, out_host + k);
+    }
   });
 }

@@ -115,7 +115,7 @@ static svb_matrix* stencil_rows(int ndim, const int64_t* dims, int nst, const in
   m->nrows = n;
   m->ncols = ncols;
   m->nnz = nnz;
-  m->ptr64 = nnz >= INT32_MAX;
+  m->ptr64 = want_ptr64(nnz);
   m->cols = alloc(nnz * 4, s);
   m->vals = alloc(nnz * 8, s);
   k_stencil_fill<<<grid_for(n, 256), 256, 0, s>>>(st, n, r0, cmin, ptr<int64_t>(ptr64), ptr<int>(m->cols),

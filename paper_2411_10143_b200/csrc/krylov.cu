@@ -64,6 +64,9 @@ struct svb_vecops {
 namespace svb {
 
 constexpr int KB = 256;  // threads per CTA for the Krylov kernels
+// longest restart: y (m doubles) must fit k_gm_update_x's dynamic shared
+// memory next to its 8.3 KB static triangle
+constexpr int KRYLOV_MAX_M = 24000;
 enum { S_RR = 0, S_ALPHA = 1, S_BETA = 2 };
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -180,10 +183,7 @@ __global__ void __launch_bounds__(KB) k_gm_residual(Gm G, const double* __restri
     const double beta = sqrt(tot);
     G.st->beta = beta;
     G.st->nonfinite = bad(beta);
-    for (int i = 0; i < (G.m + 1) * G.m; ++i) G.H[i] = 0.0;
-    for (int i = 0; i < G.m; ++i) G.cs[i] = G.sn[i] = 0.0;
-    for (int i = 0; i <= G.m; ++i) G.g[i] = 0.0;
-    G.g[0] = beta;
+    G.g[0] = beta;   // H, cs, sn and g[1..m] were cleared by the host's memsets
   }
 }
 
@@ -702,32 +702,44 @@ __global__ void __launch_bounds__(PB, 1) k_gm_mgs_tmem(Gm G, int j, double bnorm
   }
 }
 
-// x += V[:j+1]^T y (solver.py:215-216, 339-340).  Every CTA first solves the
-// (j+1)x(j+1) triangular system for y itself (solver.py:211-214, at most
-// ~1K flops, from H in L2), which replaces a separate one-thread launch.
+// Back substitution for y in the reference order (solver.py:211-214) on one
+// thread, from H and g in global memory: the restart lengths (j+1 > 32) whose
+// triangle does not fit the per-CTA staging of k_gm_update_x.
+__global__ void k_gm_solve_y(Gm G, int j) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int m = G.m;
+  for (int i = j; i >= 0; --i) {
+    double dot = 0.0;
+    for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * G.y[k];
+    G.y[i] = (G.g[i] - dot) / G.H[i * m + i];
+  }
+}
+
+// x += V[:j+1]^T y (solver.py:215-216, 339-340).  For j+1 <= 32 every CTA
+// first solves the (j+1)x(j+1) triangular system for y itself (solver.py:
+// 211-214, at most ~1K flops, from H in L2), which replaces a separate
+// one-thread launch; longer restarts take y from k_gm_solve_y (G.y) into
+// dynamic shared memory (ys, j+1 doubles).
 __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restrict__ x) {
-  __shared__ double ys[64];
+  extern __shared__ double ys[];
   __shared__ double hs[32 * 32 + 32];   // the (j+1)^2 triangle of H and g, staged once
   const int m = G.m, nj = j + 1;
   if (nj <= 32) {
     for (int t = threadIdx.x; t < nj * nj; t += blockDim.x) hs[t] = G.H[(t / nj) * m + (t % nj)];
     for (int t = threadIdx.x; t < nj; t += blockDim.x) hs[nj * nj + t] = G.g[t];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // back substitution in the reference order (solver.py:211-214)
-    for (int i = j; i >= 0; --i) {
-      double dot = 0.0;
-      if (nj <= 32) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // back substitution in the reference order (solver.py:211-214)
+      for (int i = j; i >= 0; --i) {
+        double dot = 0.0;
         for (int k = i + 1; k <= j; ++k) dot += hs[i * nj + k] * ys[k];
         ys[i] = (hs[nj * nj + i] - dot) / hs[i * nj + i];
-      } else {
-        for (int k = i + 1; k <= j; ++k) dot += G.H[i * m + k] * ys[k];
-        ys[i] = (G.g[i] - dot) / G.H[i * m + i];
       }
+      if (blockIdx.x == 0)
+        for (int i = 0; i <= j; ++i) G.y[i] = ys[i];
     }
-    if (blockIdx.x == 0)
-      for (int i = 0; i <= j; ++i) G.y[i] = ys[i];
+  } else {
+    for (int t = threadIdx.x; t < nj; t += blockDim.x) ys[t] = G.y[t];
   }
   __syncthreads();
   for_pairs(
@@ -1074,7 +1086,8 @@ extern "C" {
 
 int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
   return guard([&] {
-    SVB_REQUIRE(n >= 1 && m >= 0 && m <= 63, SVB_INVALID, "krylov workspace: n >= 1, 0 <= m <= 63");
+    SVB_REQUIRE(n >= 1 && m >= 0 && m <= KRYLOV_MAX_M, SVB_INVALID,
+                "krylov workspace: n >= 1, 0 <= restart m <= 24000");
     cudaStream_t s = 0;
     auto k = new svb_krylov();
     k->n = n;
@@ -1227,6 +1240,12 @@ int svb_gmres_restart(svb_krylov* k, void* stream) {
     SVB_REQUIRE(k->m >= 1, SVB_INVALID, "GMRES workspace needs restart m >= 1");
     k->normalized = -1;
     Gm G = gm_of(k);
+    cudaStream_t s = S(stream);
+    const size_t mm = (size_t)k->m;
+    SVB_CUDA_TRY(cudaMemsetAsync(G.H, 0, (mm + 1) * mm * 8, s));
+    SVB_CUDA_TRY(cudaMemsetAsync(G.cs, 0, mm * 8, s));
+    SVB_CUDA_TRY(cudaMemsetAsync(G.sn, 0, mm * 8, s));
+    SVB_CUDA_TRY(cudaMemsetAsync(G.g, 0, (mm + 1) * 8, s));
     k_gm_residual<<<k->rgrid, KB, 0, S(stream)>>>(G, ptr<double>(k->b), ptr<double>(k->tmp));
     SVB_CHECK_LAUNCH();
     mark(k, S(stream));
@@ -1306,8 +1325,19 @@ int svb_gmres_normalize(svb_krylov* k, int32_t j, void* stream) {
 
 int svb_gmres_update_x(svb_krylov* k, int32_t j, void* stream) {
   return guard([&] {
+    SVB_REQUIRE(j >= 0 && j < k->m, SVB_INVALID, "Arnoldi column out of range");
     Gm G = gm_of(k);
-    k_gm_update_x<<<k->rgrid, KB, 0, S(stream)>>>(G, j, ptr<double>(k->x));
+    const int nj = j + 1;
+    size_t dyn = 32 * sizeof(double);
+    if (nj > 32) {
+      k_gm_solve_y<<<1, 32, 0, S(stream)>>>(G, j);
+      SVB_CHECK_LAUNCH();
+      dyn = (size_t)nj * sizeof(double);
+      // opt in to the dynamic smem range (per device; a cheap host call)
+      SVB_CUDA_TRY(cudaFuncSetAttribute(k_gm_update_x, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(KRYLOV_MAX_M * sizeof(double) + 8)));
+    }
+    k_gm_update_x<<<k->rgrid, KB, dyn, S(stream)>>>(G, j, ptr<double>(k->x));
     SVB_CHECK_LAUNCH();
   });
 }

@@ -4,6 +4,8 @@
 // with the reference's error messages lives in the Python layer.
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+#include <climits>
 #include <cstring>
 #include <thread>
 
@@ -193,6 +195,62 @@ Buf ptr_to_rows(const svb_matrix* m, cudaStream_t s) {
     SVB_CHECK_LAUNCH();
   }
   return r;
+}
+
+
+// ---------------------------------------------------------------------------
+// host slabs of a row-partitioned rank (distributed_solve_slab)
+// ---------------------------------------------------------------------------
+// min / max of the column indices (atomics on one pair per CTA)
+template <class C>
+__global__ void k_col_minmax(const C* __restrict__ c, int64_t n, long long* __restrict__ mm) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = (long long)c[i];
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, (long long)__shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, (long long)__shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+// global -> window-relative int32 columns (in place when C is int32)
+template <class C>
+__global__ void k_cols_rebase(const C* __restrict__ src, int32_t* __restrict__ dst, int64_t n, int64_t shift) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int32_t)((int64_t)src[i] - shift);
+}
+
+// CsrMatrix structure rules (formats.py:113-138) on the device: flags[0]
+// row_ptr decreasing, flags[1] columns not strictly increasing in a row
+template <class P>
+__global__ void k_csr_check(int64_t nrows, const P* __restrict__ ptr, const int32_t* __restrict__ cols,
+                            int* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = (int64_t)ptr[i], e = (int64_t)ptr[i + 1];
+    if (e < s) {
+      flags[0] = 1;
+      continue;
+    }
+    for (int64_t k = s + 1; k < e; ++k)
+      if (cols[k] <= cols[k - 1]) {
+        flags[1] = 1;
+        break;
+      }
+  }
+}
+
+// window-relative int32 columns -> global int32 (export)
+__global__ void k_cols_shift(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n, int64_t shift) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int32_t)((int64_t)src[i] + shift);
 }
 
 }  // namespace svb
@@ -395,7 +453,7 @@ int svb_coo_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
     auto m = new svb_matrix();
     m->fmt = SVB_COO;
     m->nrows = nrows; m->ncols = ncols; m->nnz = nnz;
-    m->ptr64 = nnz >= INT32_MAX;
+    m->ptr64 = want_ptr64(nnz);
     m->rows = upload_i32(rows_host, nnz, s);
     m->cols = upload_i32(cols_host, nnz, s);
     m->vals = upload(vals_host, nnz * 8, s);
@@ -413,13 +471,112 @@ int svb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row
     auto m = new svb_matrix();
     m->fmt = SVB_CSR;
     m->nrows = nrows; m->ncols = ncols; m->nnz = nnz;
-    m->ptr64 = nnz >= INT32_MAX;
+    m->ptr64 = want_ptr64(nnz);
     if (m->ptr64) m->ptr = upload(row_ptr_host, (nrows + 1) * 8, s);
     else m->ptr = upload_i32(row_ptr_host, nrows + 1, s);
     m->cols = upload_i32(col_idx_host, nnz, s);
     m->vals = upload(vals_host, nnz * 8, s);
     SVB_CUDA_TRY(cudaStreamSynchronize(s));
     *out = publish(m);
+  });
+}
+
+int svb_csr_create_slab(int64_t nrows, int64_t ncols_global, int64_t nnz, int64_t r0, const int64_t* row_ptr_host,
+                        const void* col_idx_host, int32_t cols_i64, const double* vals_host, void* stream,
+                        int64_t* window, svb_matrix** out) {
+  return guard([&] {
+    require_index_range(nrows, ncols_global);
+    SVB_REQUIRE(r0 >= 0 && r0 + nrows <= ncols_global, SVB_DIM_MISMATCH, "slab rows outside the matrix");
+    SVB_REQUIRE(nnz >= 0 && window && out, SVB_INVALID, "slab: null output or negative nnz");
+    SVB_REQUIRE(row_ptr_host[0] == 0 && row_ptr_host[nrows] == nnz, SVB_DIM_MISMATCH,
+                "row_ptr endpoints must be 0 and nnz");
+    cudaStream_t s = S(stream);
+    std::unique_ptr<svb_matrix> m(new svb_matrix());
+    m->fmt = SVB_CSR;
+    m->nrows = nrows;
+    m->nnz = nnz;
+    m->ptr64 = want_ptr64(nnz);
+    m->ptr = m->ptr64 ? upload(row_ptr_host, (nrows + 1) * 8, s) : upload_i32(row_ptr_host, nrows + 1, s);
+    // columns: the global indices land in a staging buffer (int64) or in
+    // place (int32); their hull with the own rows is the rank's window
+    Buf stage;
+    if (cols_i64) stage = upload(col_idx_host, nnz * 8, s);
+    m->cols = cols_i64 ? alloc(nnz * 4, s) : upload(col_idx_host, nnz * 4, s);
+    Buf mm = alloc(16 + 8, s);
+    long long init[2] = {LLONG_MAX, LLONG_MIN};
+    SVB_CUDA_TRY(cudaMemcpyAsync(mm->ptr, init, 16, cudaMemcpyHostToDevice, s));
+    if (nnz > 0) {
+      if (cols_i64)
+        k_col_minmax<int64_t><<<grid_for(nnz, 256, 4), 256, 0, s>>>(ptr<int64_t>(stage), nnz, ptr<long long>(mm));
+      else
+        k_col_minmax<int32_t><<<grid_for(nnz, 256, 4), 256, 0, s>>>(ptr<int32_t>(m->cols), nnz, ptr<long long>(mm));
+      SVB_CHECK_LAUNCH();
+    }
+    long long got[2];
+    SVB_CUDA_TRY(cudaMemcpyAsync(got, mm->ptr, 16, cudaMemcpyDeviceToHost, s));
+    m->vals = upload(vals_host, nnz * 8, s);   // the H2D of values overlaps nothing else; keep it queued
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (nnz > 0)
+      SVB_REQUIRE(got[0] >= 0 && got[1] < ncols_global, SVB_DIM_MISMATCH, "column index out of range");
+    const int64_t cmin = nnz > 0 ? std::min<int64_t>(got[0], r0) : r0;
+    const int64_t cmax = nnz > 0 ? std::max<int64_t>(got[1], r0 + nrows - 1) : r0 + nrows - 1;
+    SVB_REQUIRE(cmax - cmin + 1 < INT32_MAX, SVB_INAPPLICABLE,
+                "slab column window >= 2^31 is not supported by the int32 device index layout");
+    if (nnz > 0 && (cols_i64 || cmin != 0)) {
+      if (cols_i64)
+        k_cols_rebase<int64_t><<<grid_for(nnz, 256), 256, 0, s>>>(ptr<int64_t>(stage), ptr<int32_t>(m->cols), nnz, cmin);
+      else
+        k_cols_rebase<int32_t><<<grid_for(nnz, 256), 256, 0, s>>>(ptr<int32_t>(m->cols), ptr<int32_t>(m->cols), nnz, cmin);
+      SVB_CHECK_LAUNCH();
+    }
+    stage.reset();
+    m->ncols = cmax - cmin + 1;
+    int* flags = reinterpret_cast<int*>(mm->ptr);
+    SVB_CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
+    if (m->ptr64)
+      k_csr_check<int64_t><<<grid_for(nrows, 256), 256, 0, s>>>(nrows, ptr<int64_t>(m->ptr), ptr<int32_t>(m->cols), flags);
+    else
+      k_csr_check<int32_t><<<grid_for(nrows, 256), 256, 0, s>>>(nrows, ptr<int32_t>(m->ptr), ptr<int32_t>(m->cols), flags);
+    SVB_CHECK_LAUNCH();
+    int fl[2];
+    SVB_CUDA_TRY(cudaMemcpyAsync(fl, flags, 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    SVB_REQUIRE(!fl[0], SVB_DIM_MISMATCH, "row_ptr must be non-decreasing");
+    SVB_REQUIRE(!fl[1], SVB_DIM_MISMATCH, "columns not strictly increasing within a row");
+    window[0] = cmin;
+    window[1] = cmax;
+    *out = publish(m.release());
+  });
+}
+
+int svb_csr_export(const svb_matrix* m, int64_t col_shift, int64_t* row_ptr_host, int32_t* cols_host,
+                   double* vals_host, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(m && m->fmt == SVB_CSR, SVB_UNSUPPORTED_CONFIG, "export needs a CSR matrix");
+    cudaStream_t s = S(stream);
+    {
+      Buf p64 = alloc((m->nrows + 1) * 8, s);
+      ptr_to_i64(m, ptr<int64_t>(p64), s);
+      SVB_CUDA_TRY(cudaMemcpyAsync(row_ptr_host, p64->ptr, (m->nrows + 1) * 8, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    // chunked: shift a piece of the columns on the device, copy it down
+    constexpr int64_t CH = int64_t(1) << 27;   // 128 Mi entries (512 MB)
+    Buf tmp = col_shift ? alloc(std::min(m->nnz, CH) * 4 + 4, s) : Buf();
+    for (int64_t o = 0; o < m->nnz; o += CH) {
+      const int64_t c = std::min(CH, m->nnz - o);
+      const int32_t* src = ptr<int32_t>(m->cols) + o;
+      if (col_shift) {
+        k_cols_shift<<<grid_for(c, 256), 256, 0, s>>>(src, ptr<int32_t>(tmp), c, col_shift);
+        SVB_CHECK_LAUNCH();
+        src = ptr<int32_t>(tmp);
+      }
+      SVB_CUDA_TRY(cudaMemcpyAsync(cols_host + o, src, c * 4, cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    if (m->nnz)
+      SVB_CUDA_TRY(cudaMemcpyAsync(vals_host, m->vals->ptr, m->nnz * 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
   });
 }
 
@@ -445,7 +602,7 @@ int svb_csr_row_slice(const svb_matrix* src, int64_t r0, int64_t r1, void* strea
     auto m = new svb_matrix();
     m->fmt = SVB_CSR;
     m->nrows = r1 - r0; m->ncols = src->ncols; m->nnz = b[1] - b[0];
-    m->ptr64 = m->nnz >= INT32_MAX;
+    m->ptr64 = want_ptr64(m->nnz);
     const int64_t n1 = m->nrows + 1;
     m->ptr = alloc(n1 * (m->ptr64 ? 8 : 4), s);
     const int g = grid_for(n1, 256);
@@ -453,6 +610,8 @@ int svb_csr_row_slice(const svb_matrix* src, int64_t r0, int64_t r1, void* strea
       k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int64_t>(src->ptr) + r0, ptr<int64_t>(m->ptr), n1);
     else if (src->ptr64)
       k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int64_t>(src->ptr) + r0, ptr<int32_t>(m->ptr), n1);
+    else if (m->ptr64)   // SPMVTUNE_FORCE_PTR64 on an int32 source
+      k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int32_t>(src->ptr) + r0, ptr<int64_t>(m->ptr), n1);
     else
       k_rebase_ptr<<<g, 256, 0, s>>>(ptr<int32_t>(src->ptr) + r0, ptr<int32_t>(m->ptr), n1);
     SVB_CHECK_LAUNCH();

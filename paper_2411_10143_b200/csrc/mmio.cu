@@ -377,7 +377,7 @@ extern "C" int svb_coo_from_triplets(int64_t nrows, int64_t ncols, int64_t n, co
       nruns = exclusive_scan_total(ptr<int64_t>(head), ptr<int64_t>(pos), n, s);
     }
     m->nnz = nruns;
-    m->ptr64 = nruns >= INT32_MAX;
+    m->ptr64 = want_ptr64(nruns);
     m->rows = alloc(nruns * 4, s);
     m->cols = alloc(nruns * 4, s);
     m->vals = alloc(nruns * 8, s);

@@ -140,10 +140,14 @@ class DeviceVector:
 
 
 def copy(dst: int, src: int, nbytes: int, stream: Stream | None = None) -> None:
+    if int(nbytes) == 0:         # zero-length vectors (a rank without rows) have no pointer
+        return
     _lib.check(_lib.lib().svb_copy(dst, src, int(nbytes), stream.handle if stream else None))
 
 
 def memset(dst: int, value: int, nbytes: int, stream: Stream | None = None) -> None:
+    if int(nbytes) == 0:
+        return
     _lib.check(_lib.lib().svb_memset(dst, value, int(nbytes), stream.handle if stream else None))
 
 

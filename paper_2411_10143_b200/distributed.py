@@ -40,7 +40,8 @@ from .kernels import Library, SpmvConfig, default_workers, launch
 
 __all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
            "NcclComm", "HostStagedComm", "interior_rows", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
-           "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve"]
+           "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve",
+           "slab_block", "device_diag_offsets", "distributed_solve_slab"]
 
 
 # ---------------------------------------------------------------------------
@@ -142,6 +143,8 @@ def stencil_block(dims, offsets, weights, r0: int, r1: int, stream=None) -> "Loc
     """Rank-local block of a stencil matrix generated on this rank's GPU
     (svb_csr_stencil_rows); no host copy of the rows is made."""
     import ctypes
+    if int(r1) == int(r0):
+        return _empty_block(int(r0), int(np.prod([int(d) for d in dims])))
     cmin, cmax, present = stencil_block_window(dims, offsets, r0, r1)
     d = np.ascontiguousarray(dims, dtype=np.int64)
     o = np.ascontiguousarray(offsets, dtype=np.int32).reshape(-1)
@@ -155,6 +158,63 @@ def stencil_block(dims, offsets, weights, r0: int, r1: int, stream=None) -> "Loc
     blk = LocalBlock(int(r0), int(r1), int(cmin), int(cmax), None, None, None,
                      int(np.prod(d)), present)
     blk._dev_csr = CsrMatrix._wrap(dev)
+    return blk
+
+
+def slab_block(r0: int, r1: int, ncols: int, row_ptr, col_idx, values, stream=None) -> "LocalBlock":
+    """Rank-local block from this rank's own HOST slab: rows [r0, r1) with a
+    slab-local row pointer (int64), GLOBAL column indices (int64, the
+    reference's dtype, or int32) and float64 values.  The slab is uploaded
+    and validated on the device (svb_csr_create_slab: CsrMatrix rules,
+    formats.py:113-138), its column window is the hull of its columns and
+    own rows, and its global diagonal offsets come from the device bitmap
+    (svb_diag_offsets) — the host never scans the slab."""
+    nloc = int(r1) - int(r0)
+    if nloc == 0:
+        return _empty_block(int(r0), int(ncols))
+    p = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    c = np.asarray(col_idx)
+    if c.dtype not in (np.int32, np.int64):
+        c = c.astype(np.int64)
+    c = np.ascontiguousarray(c)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if p.size != nloc + 1:
+        raise ValueError("row_ptr must have nrows+1 entries")
+    if c.size != v.size:
+        raise ValueError("col_idx and values must have equal length")
+    L = _lib.lib()
+    win = (ctypes.c_int64 * 2)()
+    from .formats import _new_handle
+    dev = _new_handle(L.svb_csr_create_slab, nloc, int(ncols), int(v.size), int(r0), p.ctypes.data,
+                      c.ctypes.data, 1 if c.dtype == np.int64 else 0, v.ctypes.data,
+                      stream.handle if stream is not None else None, win)
+    csr = CsrMatrix._wrap(dev)
+    cmin, cmax = int(win[0]), int(win[1])
+    offs = device_diag_offsets(csr, cmin - int(r0), stream)
+    blk = LocalBlock(int(r0), int(r1), cmin, cmax, None, None, None, int(ncols), offs)
+    blk._dev_csr = csr
+    return blk
+
+
+def device_diag_offsets(csr: CsrMatrix, shift: int, stream=None) -> np.ndarray:
+    """Sorted distinct diagonal offsets (col - row) of a device CSR plus
+    ``shift`` (svb_diag_offsets)."""
+    L = _lib.lib()
+    cnt = ctypes.c_int64()
+    h = stream.handle if stream is not None else None
+    _lib.check(L.svb_diag_offsets(csr._device().handle, int(shift), None, 0, ctypes.byref(cnt), h))
+    out = np.empty(max(1, cnt.value), dtype=np.int64)
+    _lib.check(L.svb_diag_offsets(csr._device().handle, int(shift),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), out.size,
+                                  ctypes.byref(cnt), h))
+    return out[:cnt.value]
+
+
+def _empty_block(r0: int, ncols: int) -> "LocalBlock":
+    """A rank that owns no rows (world > planes, or very heavy rows): it
+    joins every collective with zero-length vectors and no matrix."""
+    blk = LocalBlock(r0, r0, r0, r0 - 1, None, None, None, int(ncols), np.zeros(0, np.int64))
+    blk._dev_csr = None
     return blk
 
 
@@ -328,9 +388,19 @@ class CudaOps:
         return np.ctypeslib.as_array((ctypes.c_double * count).from_address(self._pin)).copy()
 
     def spmv(self, mat, cfg: SpmvConfig, window, dst):
+        if mat is None:          # a rank without rows
+            return
+        from .solver import DeviceOptions
+        timer = DeviceOptions.current().timer    # bench.py: CUDA events around each launch
+        if timer is not None:
+            timer.begin("spmv:" + cfg.token(), self.stream.handle)
         launch(cfg, mat, window.ptr, dst.ptr, workers=default_workers(), stream=self.stream)
+        if timer is not None:
+            timer.end("spmv:" + cfg.token(), self.stream.handle)
 
-    def local_csr(self, block: LocalBlock) -> CsrMatrix:
+    def local_csr(self, block: LocalBlock) -> CsrMatrix | None:
+        if block.nloc == 0:
+            return None
         m = getattr(block, "_dev_csr", None)
         if m is None:
             m = CsrMatrix(block.nloc, block.window, block.row_ptr, block.cols, block.values)
@@ -339,6 +409,8 @@ class CudaOps:
 
     def prepare(self, block: LocalBlock, cfg: SpmvConfig):
         csr = self.local_csr(block)
+        if csr is None:
+            return None
         return csr if cfg.format is FormatTag.CSR else convert(csr, cfg.format)
 
     def prepare_rows(self, block: LocalBlock, cfg: SpmvConfig, a: int, b: int):
@@ -721,14 +793,17 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
 # ---------------------------------------------------------------------------
 def global_features(block: LocalBlock, nrows: int, ncols: int, nnz: int, comm, local_matrix,
                     stream=None) -> FeatureVector:
-    agg = device_aggregates(local_matrix, stream)  # local rows; cols window-relative
+    # local rows; cols window-relative.  A rank without rows contributes
+    # nothing and is left out of the min (features.py:97 takes the min over
+    # the matrix's rows, not over ranks)
+    agg = device_aggregates(local_matrix, stream) if block.nloc > 0 else (0, 0, 0, None, 0, 0, 0)
     # span and run lengths are translation invariant; row-length stats are exact
     sums = comm.allgather_obj((agg[0], agg[1], agg[2], agg[3], agg[4], agg[5],
                                block.offsets.tolist()))
     s_r = sum(a[0] for a in sums)
     s_r2 = sum(a[1] for a in sums)
     mx = max(a[2] for a in sums)
-    mn = min(a[3] for a in sums)
+    mn = min(a[3] for a in sums if a[3] is not None)
     span = sum(a[4] for a in sums)
     runs = sum(a[5] for a in sums)
     ndiag = len(set().union(*[set(a[6]) for a in sums]))
@@ -757,15 +832,16 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
     csr = ops.local_csr(blk)
     # b = A * 1 on this rank's rows (a window of ones times the local rows),
     # outside the clock as in the reference (solver.py:355-358)
-    ones = ops.vec(blk.window)
-    _lib.check(_lib.lib().svb_fill(ones.ptr, blk.window, 1.0, stream.handle))
     bvec = ops.vec()
-    _lib.check(_lib.lib().svb_spmv_sequential(csr._device().handle, ones.ptr, bvec.ptr, stream.handle))
-    del ones
+    if csr is not None:
+        ones = ops.vec(blk.window)
+        _lib.check(_lib.lib().svb_fill(ones.ptr, blk.window, 1.0, stream.handle))
+        _lib.check(_lib.lib().svb_spmv_sequential(csr._device().handle, ones.ptr, bvec.ptr, stream.handle))
+        del ones
     stream.sync()
     t0 = time.perf_counter()
     cfg = initial_config or SpmvConfig(FormatTag.CSR, Library.LIB_B)
-    nnz = int(sum(comm.allgather_obj(int(csr.nnz))))
+    nnz = int(sum(comm.allgather_obj(int(csr.nnz) if csr is not None else 0)))
     if models is not None:
         from .inference import cascade_predict
         fv = global_features(blk, n, n, nnz, comm, csr, stream)
@@ -811,3 +887,51 @@ def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=N
     res["interior_rows"] = A.split
     res["x"] = ops.fetch(res["x"])
     return res, bounds
+
+
+def distributed_solve_slab(method: str, r0: int, r1: int, n: int, row_ptr, col_idx, values, b_local,
+                           params, models=None, initial_config: SpmvConfig | None = None,
+                           timings: dict | None = None, comm_class=None):
+    """Row-partitioned solve where every rank passes only ITS OWN host slab
+    (rows [r0, r1) of an n x n matrix: slab-local row_ptr, global col_idx,
+    values, and b[r0:r1]) — the form a caller holding a matrix too large for
+    one host (config 5: 94.7 GB as int64 CSR) uses.  Per call: the slab is
+    uploaded and validated on the device, the cascade runs on the exact
+    global features, the local block is converted, the solve runs, and the
+    local slice of x comes back to the host.  Returns the report dict
+    (``x`` = this rank's host slice)."""
+    import time
+
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    stream = device.thread_stream(0)
+    t0 = time.perf_counter()
+    blk = slab_block(r0, r1, n, row_ptr, col_idx, values, stream)
+    ops, comm = CudaOps(blk.nloc, stream), (comm_class or NcclComm)(stream)
+    rows = comm.allgather_obj((int(r0), int(r1)))
+    bounds = np.asarray([rows[0][0]] + [r[1] for r in rows], dtype=np.int64)
+    if bounds[0] != 0 or bounds[-1] != n or any(rows[k][1] != rows[k + 1][0] for k in range(world - 1)):
+        raise ValueError("rank slabs must tile rows [0, n) in rank order")
+    csr = ops.local_csr(blk)
+    t1 = time.perf_counter()
+    cfg = initial_config or SpmvConfig(FormatTag.CSR, Library.LIB_B)
+    nnz = int(sum(comm.allgather_obj(int(csr.nnz) if csr is not None else 0)))
+    if models is not None:
+        from .inference import cascade_predict
+        fv = global_features(blk, n, n, nnz, comm, csr, stream)
+        cfg = cascade_predict(models, fv)
+    t2 = time.perf_counter()
+    A = DistOperator(blk, bounds, comm, ops, cfg)
+    stream.sync()
+    t3 = time.perf_counter()
+    res = (dist_cg if method == "cg" else dist_gmres)(A, np.ascontiguousarray(b_local, dtype=np.float64),
+                                                       params)
+    res["x"] = ops.fetch(res["x"])
+    t4 = time.perf_counter()
+    res["config"] = cfg.token()
+    res["interior_rows"] = A.split
+    res["rank"] = rank
+    if timings is not None:
+        timings.update({"upload_s": t1 - t0, "predict_s": t2 - t1, "convert_s": t3 - t2,
+                        "solve_s": t4 - t3, "total_s": t4 - t0})
+    return res

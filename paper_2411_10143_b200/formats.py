@@ -203,6 +203,21 @@ class CooMatrix(_Resident):
         return cls(nrows, ncols, r, c, v)
 
 
+    @classmethod
+    def from_triplets_device(cls, nrows, ncols, rows, cols, values, *, sum_duplicates=False):
+        """``from_triplets`` with the sort (stable radix sort) and the
+        duplicate merge (np.add.reduceat order) on the device
+        (svb_coo_from_triplets); the result stays device-resident."""
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if not (r.size == c.size == v.size):
+            raise ValueError("rows, cols and values must have equal length")
+        dev = _new_handle(_lib.lib().svb_coo_from_triplets, int(nrows), int(ncols), int(r.size),
+                          r.ctypes.data, c.ctypes.data, v.ctypes.data, 1 if sum_duplicates else 0, None)
+        return cls._wrap(dev)
+
+
 class CsrMatrix(_Resident):
     """Compressed sparse rows; columns strictly increasing within each row
     (formats.py:103-146)."""

@@ -121,6 +121,26 @@ def _is_device_buffer(a) -> bool:
     return getattr(a, "is_cuda", False)              # torch CUDA tensor
 
 
+def _device_operand(a, name: str) -> tuple[int, str]:
+    """(length, "float32"|"float64") of a device SpMV operand; raises
+    ValueError for any other dtype, a non-contiguous tensor or a tensor on
+    another device than the current one."""
+    if hasattr(a, "n"):                                  # DeviceVector: flat by construction
+        kind = np.dtype(a.dtype).name
+        n = a.n
+    else:
+        kind = str(a.dtype).replace("torch.", "")
+        if a.dim() != 1 or not a.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D device vector")
+        dev = _lib.device_index()
+        if a.device.index is not None and a.device.index != dev:
+            raise ValueError(f"{name} lives on {a.device}, not the library's device cuda:{dev}")
+        n = a.numel()
+    if kind not in ("float32", "float64"):
+        raise ValueError(f"{name} must be float32 or float64, got {kind}")
+    return n, kind
+
+
 def launch(cfg: SpmvConfig, m, x_ptr: int, y_ptr: int, *, workers: int, f32: bool = False,
            stream=None) -> None:
     """Enqueue y = A x on ``stream`` with raw device pointers (no checks
@@ -144,16 +164,25 @@ def execute_spmv(cfg: SpmvConfig, m, x, *, workers: int | None = None, out=None,
         raise UnsupportedConfigError(
             f"matrix is stored as {format_of(m).value}, kernel expects {cfg.format.value}")
     if _is_device_buffer(x):
-        n_x = x.n if hasattr(x, "n") else x.numel()
+        n_x, kind_x = _device_operand(x, "x")
         if n_x != m.ncols:
             raise ValueError(f"x must have length {m.ncols}, got ({n_x},)")
-        f32 = str(getattr(x, "dtype", "float64")).endswith("float32")
+        f32 = kind_x == "float32"
         if out is None:
             if hasattr(x, "n"):
                 from .device import DeviceVector
                 out = DeviceVector(m.nrows, np.float32 if f32 else np.float64)
             else:
                 out = x.new_empty(m.nrows)
+        else:
+            # the kernel writes raw pointers: a short, mistyped or strided
+            # out would be silent device-memory corruption
+            if not _is_device_buffer(out):
+                raise ValueError("out must be a device buffer when x is one")
+            n_o, kind_o = _device_operand(out, "out")
+            if n_o != m.nrows or kind_o != kind_x:
+                raise ValueError(f"out must be a {kind_x} vector of length {m.nrows}, "
+                                 f"got {kind_o} of length {n_o}")
         launch(cfg, m, _lib.ptr(x) if not hasattr(x, "n") else x.ptr,
                _lib.ptr(out) if not hasattr(out, "n") else out.ptr, workers=workers, f32=f32,
                stream=stream)

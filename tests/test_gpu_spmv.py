@@ -6,6 +6,8 @@ reference produced (tests/golden, generated from /root/reference); COO/LibB
 reference's 1e-8 bar.  Larger matrices are checked against the CPU oracle
 bit-for-bit, fp32 against fp64 at fp32 tolerance.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -77,21 +79,81 @@ def test_larger_matrices_against_oracle(gen):
     assert rel(got, O.spmv_sequential(ocsr, x)) <= 1e-12
 
 
-def test_fp32_kernels_against_fp64():
-    n, m, ptr, cols, vals = G.powerlaw_spd(20000, seed=2)
+FP32_TOL = 1e-5   # fp32 SpMV vs the fp64 result, relative 2-norm (fp32 values, x and sums)
+
+
+@pytest.mark.parametrize("gen", ["powerlaw", "convdiff", "banded"])
+def test_fp32_kernels_against_fp64(gen):
+    """fp32 SpMV of every configuration the matrix admits (north star:
+    "fp64/fp32 SpMV for every format") — DIA included on the banded and
+    stencil matrices (the power-law one has too many diagonals)."""
+    if gen == "powerlaw":
+        n, m, ptr, cols, vals = G.powerlaw_spd(20000, seed=2)
+    elif gen == "convdiff":
+        n, m, ptr, cols, vals = G.convdiff9(150)
+    else:
+        n, m, ptr, cols, vals = G.banded(30000, [-700, -3, -1, 0, 2, 9, 1500], seed=4, diagonal_boost=3.0)
     csr = P.CsrMatrix(n, m, ptr, cols, vals)
     x = np.random.default_rng(5).uniform(0.5, 1.5, size=m)
     s = device.thread_stream()
     x32 = device.DeviceVector.from_numpy(x.astype(np.float32), s)
     x64 = device.DeviceVector.from_numpy(x, s)
+    seen = set()
     for cfg in P.enumerate_configs():
-        rep = P.convert(csr, cfg.format) if cfg.format is not P.FormatTag.DIA else None
-        if rep is None:
+        try:
+            rep = P.convert(csr, cfg.format)
+        except P.FormatInapplicableError:
+            assert gen == "powerlaw" and cfg.format is P.FormatTag.DIA
             continue
         y64 = P.execute_spmv(cfg, rep, x64, stream=s).to_numpy(s)
         y32 = P.execute_spmv(cfg, rep, x32, stream=s).to_numpy(s)
         assert y32.dtype == np.float32
-        assert rel(y32.astype(np.float64), y64) <= 1e-5, cfg.token()
+        assert rel(y32.astype(np.float64), y64) <= FP32_TOL, cfg.token()
+        seen.add(cfg.format)
+    assert len(seen) == (4 if gen == "powerlaw" else 5)
+
+
+def test_ptr64_mode_is_what_the_environment_asks():
+    """tests/test_gpu_scale.py re-runs this module with SPMVTUNE_FORCE_PTR64=1:
+    the int64 row-pointer kernels must then really be the ones running."""
+    n, m, ptr, cols, vals = G.poisson2d(20)
+    A = P.CsrMatrix(n, m, ptr, cols, vals)
+    forced = os.environ.get("SPMVTUNE_FORCE_PTR64") == "1"
+    assert bool(A._device().info.ptr64) == forced
+    assert bool(P.convert(P.to_coo(A), P.FormatTag.CSR)._device().info.ptr64) == forced
+
+
+class TestDeviceOutValidation:
+    """Raw-pointer kernels must never see a short, mistyped or strided
+    buffer (silent device-memory corruption)."""
+
+    def setup_method(self):
+        n, m, ptr, cols, vals = G.poisson2d(12)
+        self.A = P.CsrMatrix(n, m, ptr, cols, vals)
+        self.cfg = P.SpmvConfig(P.FormatTag.CSR, P.Library.LIB_B)
+
+    def test_short_or_mistyped_out(self):
+        torch = pytest.importorskip("torch")
+        x = torch.rand(self.A.ncols, dtype=torch.float64, device="cuda")
+        for bad in (torch.empty(self.A.nrows - 1, dtype=torch.float64, device="cuda"),
+                    torch.empty(self.A.nrows, dtype=torch.float32, device="cuda"),
+                    torch.empty(self.A.nrows, dtype=torch.float16, device="cuda"),
+                    np.empty(self.A.nrows)):
+            with pytest.raises(ValueError):
+                P.execute_spmv(self.cfg, self.A, x, out=bad)
+        y = torch.full((self.A.nrows,), 7.0, dtype=torch.float64, device="cuda")
+        assert P.execute_spmv(self.cfg, self.A, x, out=y) is y
+
+    def test_bad_x(self):
+        torch = pytest.importorskip("torch")
+        with pytest.raises(ValueError):
+            P.execute_spmv(self.cfg, self.A, torch.ones(self.A.ncols, dtype=torch.int64, device="cuda"))
+        with pytest.raises(ValueError):
+            P.execute_spmv(self.cfg, self.A, torch.rand(2 * self.A.ncols, dtype=torch.float64,
+                                                        device="cuda")[::2])
+        dv = device.DeviceVector(self.A.ncols, np.float64)
+        with pytest.raises(ValueError):
+            P.execute_spmv(self.cfg, self.A, dv, out=device.DeviceVector(self.A.nrows + 3))
 
 
 def test_device_buffer_path_matches_host_path():
