@@ -320,6 +320,27 @@ int svb_dcg_update(svb_vecops* v, double* sc_dev, int32_t irr, int32_t ipq, int3
                    const double* q_dev, double* x_dev, double* r_dev, void* stream);
 int svb_dcg_p(svb_vecops* v, const double* sc_dev, int32_t inew, int32_t iold, const double* r_dev,
               double* p_dev, void* stream);
+/* y = A x in the configuration, fused with *out_dev = dsrc . y (CG's p.Ap,
+ * oracle/cpu_oracle.py:cg) — one pass for DIA (the dot folded into the
+ * TMA-staged SpMV), SpMV + dot otherwise; `accumulate` adds into *out_dev
+ * (the interior / boundary row parts of one local SpMV, in a fixed order). */
+int svb_vec_spmv_dot(svb_vecops* v, const svb_matrix* m, int format, int library, int lane, int workers,
+                     const double* x_dev, double* y_dev, const double* dsrc_dev, double* out_dev,
+                     int32_t accumulate, void* stream);
+/* Row-partitioned GMRES, classical Gram-Schmidt twice (CGS2; the reference's
+ * MGS loop solver.py:294-297 needs j+2 sequential all-reduces per Arnoldi
+ * step across ranks, CGS2 two).  V = basis rows (row i at V_dev + i*ld),
+ * the first k used; h_dev, div_dev, out_dev are device scalars.  Modes:
+ *   0 DOT:    out[i] = V_i . w                                (i < k)
+ *   1 UPDATE: dst = w - sum h_i V_i; out[i] = V_i . dst; out[k] = dst . dst
+ *   2 FINISH: dst = (w - sum h_i V_i) / *div
+ *   3 AXPY:   dst = w + sum h_i V_i   (x += V y)
+ * dst may alias w.  Fixed-order sums (deterministic). */
+int svb_vec_gs(svb_vecops* v, int32_t mode, const double* V_dev, int64_t ld, int32_t k, const double* h_dev,
+               const double* div_dev, const double* w_dev, double* dst_dev, double* out_dev, void* stream);
+/* *hn_dev = sqrt(max(*nrm_dev - sum h2_i^2, 0)): the norm after CGS2's
+ * second pass from the first pass's w.w and the correction coefficients. */
+int svb_vec_gs_hn(const double* h2_dev, int32_t k, const double* nrm_dev, double* hn_dev, void* stream);
 /* x[0..n) = v on the device (row-partitioned setup: windows of ones) */
 int svb_fill(double* x_dev, int64_t n, double v, void* stream);
 

@@ -567,7 +567,7 @@ def gmres(matvec, b, restart=30, tol=1e-8, max_iters=1000, on_iteration=None) ->
     return out(fin <= tol, fin)
 
 
-def cg(matvec, b, tol=1e-8, max_iters=1000) -> dict:
+def cg(matvec, b, tol=1e-8, max_iters=1000, dot=None) -> dict:
     """Hestenes–Stiefel CG.  The reference has NO CG; this is the
     new oracle SURVEY.md §8c specifies: x0 = 0, one matvec per iteration,
     recurrence residual ||r||/||b|| as the per-iteration estimate, explicit
@@ -589,12 +589,14 @@ def cg(matvec, b, tol=1e-8, max_iters=1000) -> dict:
         return out(True, 0.0)
     if max_iters == 0:
         return out(False, None)
+    if dot is None:       # the reference's inner product (BLAS ddot via np.dot)
+        dot = np.dot
     r = b.copy()
     p = r.copy()
-    rr = float(np.dot(r, r))
+    rr = float(dot(r, r))
     while done < max_iters:
         q = matvec(p)
-        pq = float(np.dot(p, q))
+        pq = float(dot(p, q))
         if not math.isfinite(pq):
             return out(False, None, "nonfinite")
         if pq == 0.0:
@@ -603,7 +605,7 @@ def cg(matvec, b, tol=1e-8, max_iters=1000) -> dict:
         alpha = rr / pq
         x = x + alpha * p
         r = r - alpha * q
-        rr_new = float(np.dot(r, r))
+        rr_new = float(dot(r, r))
         done += 1
         est = math.sqrt(rr_new) / bnorm
         if not math.isfinite(est):
@@ -615,7 +617,7 @@ def cg(matvec, b, tol=1e-8, max_iters=1000) -> dict:
             if fin <= tol:
                 return out(True, fin)
             p = r.copy()
-            rr = float(np.dot(r, r))
+            rr = float(dot(r, r))
             continue
         p = r + (rr_new / rr) * p
         rr = rr_new

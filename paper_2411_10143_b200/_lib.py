@@ -151,6 +151,9 @@ _SIGS = {
     "svb_vec_axpy_dot": [_P, _P, _D, _P, _P, _P, _P, _P],
     "svb_vec_axpby": [_P, _D, _P, _D, _P, _P],
     "svb_vec_scale": [_P, _P, _D, _P],
+    "svb_vec_spmv_dot": [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _I32, _P],
+    "svb_vec_gs": [_P, _I32, _P, _I64, _I32, _P, _P, _P, _P, _P, _P],
+    "svb_vec_gs_hn": [_P, _I32, _P, _P, _P],
     "svb_forest_create": [_I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _PP],
     "svb_forest_destroy": [_P],
     "svb_forest_predict": [_P, _P, _P, _P],

@@ -11,6 +11,7 @@
 // "axpy_{i-1} + dot_i" passes: pass i reads w, V[i-1] and V[i] once.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -59,6 +60,9 @@ struct svb_vecops {
   int64_t n = 0;
   unsigned grid = 1;
   svb::Buf partials;  // grid doubles + reduction counter
+  svb::Buf bpart;     // block sweeps: grid x (VB+1) doubles + counter (lazy)
+  svb::Buf spart;     // fused SpMV+dot: sgrid doubles + counter (lazy)
+  unsigned sgrid = 0;
 };
 
 namespace svb {
@@ -992,6 +996,17 @@ __global__ void __launch_bounds__(KB) k_dot(int64_t n, const double* __restrict_
   if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = tot;
 }
 
+// generic dot with an accumulate mode (row parts of one local SpMV)
+__global__ void __launch_bounds__(KB) k_dot_acc(int64_t n, const double* __restrict__ a,
+                                                const double* __restrict__ b, double* partials,
+                                                unsigned* counter, double* out, int accumulate) {
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    acc += a[e] * b[e];
+  double tot;
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = accumulate ? *out + tot : tot;
+}
+
 // Row-partitioned CG, fused on device scalars sc[] (all-reduced in place
 // between the kernels): x += a p, r -= a q with a = sc[irr]/sc[ipq], and the
 // local r.r into sc[out].  A zero or non-finite p.Ap leaves x and r untouched
@@ -1052,6 +1067,112 @@ __global__ void __launch_bounds__(KB) k_dcg_p(int64_t n, const double* sc, int i
         st2(p + e, make_double2(rr.x + b * pp.x, rr.y + b * pp.y));
       },
       [&](int64_t e) { p[e] = r[e] + b * p[e]; });
+}
+
+// ---------------------------------------------------------------------------
+// Row-partitioned GMRES: classical Gram-Schmidt twice (CGS2) over a block of
+// basis rows V[r0 .. r0+k) (row stride ld, k <= VB), so an Arnoldi step needs
+// two all-reduces across ranks instead of MGS's j+2:
+//   GS_DOT:    out[i] = V_i . w
+//   GS_UPDATE: w -= sum_i h[i] V_i; out[i] = V_i . w; out[k] = w . w
+//   GS_FINISH: dst = (w - sum_i h[i] V_i) / *div
+//   GS_AXPY:   dst = w + sum_i h[i] V_i          (x += V y at a restart)
+// Each basis row is loaded once per element (registers), the k(+1) sums are
+// folded per CTA and, by the last CTA to finish, in fixed CTA order.
+// ---------------------------------------------------------------------------
+constexpr int VB = 32;
+enum { GS_DOT = 0, GS_UPDATE = 1, GS_FINISH = 2, GS_AXPY = 3 };   // C-ABI modes
+enum { K_DOT = 0, K_UPDATE = 1, K_SUB = 2, K_ADD = 3 };            // kernel modes
+
+// K_DOT:    out[i] = V_i . w (+ out[k] = w . w with `norm`)
+// K_UPDATE: t = w - sum h_i V_i -> dst; out[i] = V_i . t; out[k] = t . t
+// K_SUB:    dst = (w - sum h_i V_i) [/ *div]
+// K_ADD:    dst = w + sum h_i V_i
+template <int MODE>
+__global__ void __launch_bounds__(KB) k_gs_block(int64_t n, const double* __restrict__ V, int64_t ld, int k,
+                                                 const double* __restrict__ h, const double* __restrict__ div,
+                                                 int norm, const double* w, double* dst, double* partials,
+                                                 unsigned* counter, double* out) {
+  constexpr bool DOTS = MODE == K_DOT || MODE == K_UPDATE;
+  constexpr int NS = DOTS ? VB + 1 : 1;
+  __shared__ double hs[VB];
+  __shared__ double red[KB / 32][VB + 1];
+  __shared__ bool last;
+  if (MODE != K_DOT && threadIdx.x < k) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  const bool scale = MODE == K_SUB && div != nullptr;
+  const double dv = scale ? *div : 1.0;
+  double acc[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) acc[i] = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double v[VB];
+#pragma unroll
+    for (int i = 0; i < VB; ++i)
+      if (i < k) v[i] = __ldcs(V + (int64_t)i * ld + e);
+    double t = w[e];
+    if (MODE == K_UPDATE || MODE == K_SUB) {
+#pragma unroll
+      for (int i = 0; i < VB; ++i)
+        if (i < k) t -= hs[i] * v[i];
+    } else if (MODE == K_ADD) {
+#pragma unroll
+      for (int i = 0; i < VB; ++i)
+        if (i < k) t += hs[i] * v[i];
+    }
+    if (scale) t = t / dv;
+    if (MODE != K_DOT) dst[e] = t;
+    if (DOTS) {
+#pragma unroll
+      for (int i = 0; i < VB; ++i)
+        if (i < k) acc[i] += v[i] * t;
+      if (norm) acc[VB] += t * t;
+    }
+  }
+  if (!DOTS) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nv = k + (norm ? 1 : 0);
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    if (i < k || (i == VB && norm)) {
+      double a = acc[i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) red[wid][i < VB ? i : k] = a;   // the norm lands right after the k dots
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double b = 0.0;
+    for (int q = 0; q < KB / 32; ++q) b += red[q][threadIdx.x];
+    partials[(int64_t)blockIdx.x * (VB + 1) + threadIdx.x] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < nv) {
+    double t = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partials + (int64_t)b * (VB + 1) + threadIdx.x);
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+// hn = sqrt(max(nrm - sum h2_i^2, 0)): ||w2|| of the second CGS pass from
+// ||w1||^2 and the (tiny) re-orthogonalisation coefficients (w2 = w1 - V h2
+// with V orthonormal), so no third reduction is needed
+__global__ void k_gs_hn(const double* __restrict__ h2, int k, const double* __restrict__ nrm, double* hn) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < k; ++i) s += h2[i] * h2[i];
+  const double r = *nrm - s;
+  *hn = r > 0.0 ? sqrt(r) : 0.0;
 }
 
 __global__ void __launch_bounds__(KB) k_fill(double* __restrict__ x, int64_t n, double v) {
@@ -1491,6 +1612,103 @@ int svb_vec_axpy_dot(svb_vecops* v, const double* alpha, double sign, const doub
   return guard([&] {
     k_axpy_dot<<<v->grid, KB, 0, S(stream)>>>(v->n, alpha, sign, x, y, z, ptr<double>(v->partials), vctr(v),
                                                out);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+static double* bpart(svb_vecops* v, unsigned** ctr) {
+  if (!v->bpart) {
+    v->bpart = alloc((size_t)v->grid * (VB + 1) * 8 + 64, 0);
+    detach(v->bpart);
+    SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(v->bpart->ptr) + (size_t)v->grid * (VB + 1) * 8, 0, 64, 0));
+    SVB_CUDA_TRY(cudaStreamSynchronize(0));
+  }
+  *ctr = reinterpret_cast<unsigned*>(static_cast<char*>(v->bpart->ptr) + (size_t)v->grid * (VB + 1) * 8);
+  return ptr<double>(v->bpart);
+}
+
+// rows [0, k) of V in groups of at most VB per launch
+int svb_vec_gs(svb_vecops* v, int32_t mode, const double* V, int64_t ld, int32_t k, const double* h,
+               const double* div, const double* w, double* dst, double* out, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(k >= 1 && V && w, SVB_INVALID, "block Gram-Schmidt: k >= 1 rows and w required");
+    SVB_REQUIRE(mode >= GS_DOT && mode <= GS_AXPY, SVB_INVALID, "block Gram-Schmidt: unknown mode");
+    SVB_REQUIRE(mode == GS_DOT || (h && dst), SVB_INVALID, "block Gram-Schmidt: coefficients and dst required");
+    SVB_REQUIRE(!(mode == GS_DOT || mode == GS_UPDATE) || out, SVB_INVALID, "block Gram-Schmidt: output required");
+    SVB_REQUIRE(mode != GS_FINISH || div, SVB_INVALID, "block Gram-Schmidt: divisor required");
+    if (v->n == 0) {   // a rank without rows still produces its (zero) partials
+      if (mode == GS_DOT || mode == GS_UPDATE)
+        SVB_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)(k + (mode == GS_UPDATE)) * 8, S(stream)));
+      return;
+    }
+    cudaStream_t s = S(stream);
+    unsigned* ctr = nullptr;
+    double* part = bpart(v, &ctr);
+    auto row = [&](int g) { return V + (int64_t)g * ld; };
+    if (mode == GS_UPDATE && k <= VB) {   // fused: one pass
+      k_gs_block<K_UPDATE><<<v->grid, KB, 0, s>>>(v->n, V, ld, k, h, nullptr, 1, w, dst, part, ctr, out);
+      SVB_CHECK_LAUNCH();
+      return;
+    }
+    const double* src = w;
+    if (mode != GS_DOT) {   // apply the coefficients group by group (in row order)
+      for (int g = 0; g < k; g += VB) {
+        const int kk = std::min(VB, k - g);
+        const bool lastg = g + kk >= k;
+        if (mode == GS_AXPY)
+          k_gs_block<K_ADD><<<v->grid, KB, 0, s>>>(v->n, row(g), ld, kk, h + g, nullptr, 0, src, dst, part, ctr,
+                                                   nullptr);
+        else
+          k_gs_block<K_SUB><<<v->grid, KB, 0, s>>>(v->n, row(g), ld, kk, h + g,
+                                                   (mode == GS_FINISH && lastg) ? div : nullptr, 0, src, dst,
+                                                   part, ctr, nullptr);
+        SVB_CHECK_LAUNCH();
+        src = dst;
+      }
+      if (mode != GS_UPDATE) return;
+    }
+    // dots of the (updated) w against every row; the norm with the last group
+    for (int g = 0; g < k; g += VB) {
+      const int kk = std::min(VB, k - g);
+      const int nrm = (mode == GS_UPDATE && g + kk >= k) ? 1 : 0;
+      k_gs_block<K_DOT><<<v->grid, KB, 0, s>>>(v->n, row(g), ld, kk, nullptr, nullptr, nrm, src, nullptr, part,
+                                               ctr, out + g);
+      SVB_CHECK_LAUNCH();
+    }
+  });
+}
+
+int svb_vec_gs_hn(const double* h2, int32_t k, const double* nrm, double* hn, void* stream) {
+  return guard([&] {
+    k_gs_hn<<<1, 32, 0, S(stream)>>>(h2, k, nrm, hn);
+    SVB_CHECK_LAUNCH();
+  });
+}
+
+int svb_vec_spmv_dot(svb_vecops* v, const svb_matrix* m, int format, int library, int lane, int workers,
+                     const double* x, double* y, const double* dsrc, double* out, int32_t accumulate, void* stream) {
+  return guard([&] {
+    SVB_REQUIRE(m && out, SVB_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    if (!v->spart) {
+      v->sgrid = std::max<unsigned>(grid_for(std::max<int64_t>(v->n, 1), 256, 8), (unsigned)sm_count());
+      v->spart = alloc((size_t)v->sgrid * 8 + 64, 0);
+      detach(v->spart);
+      SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(v->spart->ptr) + (size_t)v->sgrid * 8, 0, 64, 0));
+      SVB_CUDA_TRY(cudaStreamSynchronize(0));
+    }
+    double* part = ptr<double>(v->spart);
+    unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(v->spart->ptr) + (size_t)v->sgrid * 8);
+    if (m->nrows == 0) {
+      if (!accumulate) SVB_CUDA_TRY(cudaMemsetAsync(out, 0, 8, s));
+      return;
+    }
+    if (format == SVB_DIA && m->fmt == SVB_DIA && grid_for(m->nrows, 256, 8) <= v->sgrid) {
+      launch_dia_dot(m, x, y, dsrc, part, ctr, out, nullptr, v->sgrid, s, accumulate);
+      return;
+    }
+    spmv_dispatch(m, format, library, lane, workers, SVB_F64, x, y, s);
+    k_dot_acc<<<grid_for(m->nrows, KB, 4), KB, 0, s>>>(m->nrows, dsrc, y, part, ctr, out, accumulate);
     SVB_CHECK_LAUNCH();
   });
 }

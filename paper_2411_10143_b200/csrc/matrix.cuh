@@ -87,7 +87,11 @@ void forget_bounds(const svb_matrix* m);  // drop cached LibC chunk bounds (spmv
 // DIA SpMV y = A x fused with sum dsrc.y into *out (spmv.cu, k_dia_dot);
 // partials holds >= max_grid doubles, counter is zero and left zero
 void launch_dia_dot(const svb_matrix* m, const double* x, double* y, const double* dsrc, double* partials,
-                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s);
+                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s,
+                    int accumulate = 0);
+// y = A x in any configuration (the svb_spmv dispatcher)
+void spmv_dispatch(const svb_matrix* m, int fmt, int lib, int lane, int workers, int dtype, const void* x, void* y,
+                   cudaStream_t s);
 
 // exclusive scan of int64 counts (n+1 outputs; out[n] = total) and the total
 // copied back to the host (synchronises `s`)

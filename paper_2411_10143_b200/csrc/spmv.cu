@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <type_traits>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "matrix.cuh"
@@ -736,6 +737,140 @@ __global__ void __launch_bounds__(256) k_dia(int64_t nrows, int64_t ncols, int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// DIA/LibA, offsets in the parameter space (the default for <= 32 stored
+// diagonals).  k_dia is latency-bound (ncu, config 5: long-scoreboard
+// stalls, DRAM 70 %, L2 48 %): each group of 4 diagonals first loads its
+// offsets, then data and x, then waits.  Here the offsets travel in the
+// kernel's parameter space (constant bank: nothing on the load chain) and
+// the diagonals go in groups of G = 3 — for a stencil the dx = -1, 0, +1
+// triple, whose x loads hit the same L1 lines back to back.  Measured at
+// config 5 (profiles/r2_dia_variants.json): 8.38 ms vs 8.83 ms for k_dia
+// (0.93 vs 0.88 of the copy-bandwidth peak; the 27-stream read ceiling
+// measured by profiles/mb_streams.cu is 6.87 TB/s); deeper groups (6, 9),
+// two rows per thread, per-CTA row blocks and a TMA-staged ring (tiles of
+// every diagonal bulk-copied to shared memory, x gathered by 8 consumer
+// warps) were all slower (4.1-5.6 TB/s).  With DOT the dot(dsrc, y) that
+// follows the SpMV in CG is folded in (per-CTA partials, fixed-order fold by
+// the last CTA; `accumulate` adds into *out).  Per-row operation order as
+// k_dia, so y is bit-identical.
+// ---------------------------------------------------------------------------
+struct DiaOffs {
+  long long o[32];
+};
+constexpr int DIA_REG_MAX = 32;
+
+template <class T, int G, bool DOT>
+__global__ void __launch_bounds__(256) k_dia_reg(int64_t nrows, int64_t ncols, int ndiag, DiaOffs offs,
+                                                 const T* __restrict__ data, const T* __restrict__ x,
+                                                 T* __restrict__ y, const T* __restrict__ dsrc, double* partials,
+                                                 unsigned* counter, double* out, const int* skip, int accumulate) {
+  if (DOT && skip != nullptr && *skip) return;
+  double dot = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int k0 = 0; k0 < ndiag; k0 += G) {
+      T dv[G], xv[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int k = k0 + u;
+        if (k < ndiag) {
+          const int64_t j = i + offs.o[k];
+          dv[u] = ld_stream(data + (int64_t)k * nrows + i);
+          xv[u] = (j >= 0 && j < ncols) ? ld_x(x + j) : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int k = k0 + u;
+        if (k < ndiag) {
+          const int64_t j = i + offs.o[k];
+          if (j >= 0 && j < ncols) acc = acc + dv[u] * xv[u];
+        }
+      }
+    }
+    y[i] = acc;
+    if (DOT) dot = dot + (double)dsrc[i] * (double)acc;
+  }
+  if (!DOT) return;
+  __shared__ double sh[8];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) sh[wid] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < 8; ++w) b += sh[w];
+    partials[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;   // fixed-order fold of the CTA partials by the whole CTA
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(partials + b);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  if (lane == 0) sh[wid] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < 8; ++w) g += sh[w];
+    *out = accumulate ? *out + g : g;
+    *counter = 0;
+  }
+}
+
+// Grid of a grid-stride kernel sized by its real occupancy: grid_for()'s
+// 8 CTAs/SM assumes <= 32 registers; a kernel that fits fewer would leave a
+// partial second wave doing a full share of the rows (measured: the fused
+// DIA SpMV+dot at 36 registers ran 20 % slower on a 1184-CTA grid).
+static unsigned resident_grid(const void* kern, int block, int64_t items) {
+  static std::mutex mu;
+  static std::map<const void*, int> occ;
+  int per = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find(kern);
+    if (it == occ.end()) {
+      SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, block, 0));
+      occ[kern] = per = per < 1 ? 1 : per;
+    } else {
+      per = it->second;
+    }
+  }
+  return grid_for(items, block, per);
+}
+
+// SPMVTUNE_DIA=0 pins the thread-per-row k_dia (A/B experiments)
+static bool dia_reg_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SPMVTUNE_DIA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class T, bool DOT>
+static bool launch_dia_reg(const svb_matrix* m, const T* vals, const T* x, T* y, const T* dsrc, double* partials,
+                           unsigned* counter, double* out, const int* skip, int accumulate, unsigned max_grid,
+                           cudaStream_t s) {
+  if (!dia_reg_enabled() || m->ndiag < 1 || m->ndiag > DIA_REG_MAX || m->h_offs.size() != (size_t)m->ndiag)
+    return false;
+  const unsigned g = resident_grid((const void*)k_dia_reg<T, 3, DOT>, 256, m->nrows);
+  if (DOT && g > max_grid) return false;
+  DiaOffs o{};
+  for (int k = 0; k < m->ndiag; ++k) o.o[k] = m->h_offs[k];
+  k_dia_reg<T, 3, DOT><<<g, 256, 0, s>>>(m->nrows, m->ncols, (int)m->ndiag, o, vals, x, y, dsrc, partials, counter,
+                                         out, skip, accumulate);
+  return true;
+}
+
 // DIA SpMV fused with the Krylov dot product that always follows it in CG
 // (q = A p, then p.q): the same per-row sums as k_dia (identical y), plus
 // sum_i dsrc[i] * y[i] folded per CTA and, in the last CTA to finish, over the
@@ -746,7 +881,7 @@ __global__ void __launch_bounds__(256) k_dia_dot(int64_t nrows, int64_t ncols, i
                                                  const long long* __restrict__ offs, const double* __restrict__ data,
                                                  const double* __restrict__ x, double* __restrict__ y,
                                                  const double* __restrict__ dsrc, double* partials, unsigned* counter,
-                                                 double* out, const int* skip) {
+                                                 double* out, const int* skip, int accumulate) {
   if (skip != nullptr && *skip) return;
   double dot = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
@@ -801,19 +936,25 @@ __global__ void __launch_bounds__(256) k_dia_dot(int64_t nrows, int64_t ncols, i
   if (threadIdx.x == 0) {
     double g = 0.0;
     for (int w = 0; w < 8; ++w) g += sh[w];
-    *out = g;
+    *out = accumulate ? *out + g : g;
     *counter = 0;
   }
 }
 
 void launch_dia_dot(const svb_matrix* m, const double* x, double* y, const double* dsrc, double* partials,
-                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s) {
+                    unsigned* counter, double* out, const int* skip, unsigned max_grid, cudaStream_t s,
+                    int accumulate) {
   SVB_REQUIRE(m->fmt == SVB_DIA, SVB_UNSUPPORTED_CONFIG, "fused SpMV+dot needs a DIA matrix");
   const int64_t n = m->nrows;
+  if (launch_dia_reg<double, true>(m, ptr<double>(m->vals), x, y, dsrc, partials, counter, out, skip, accumulate,
+                                   max_grid, s)) {
+    SVB_CHECK_LAUNCH();
+    return;
+  }
   unsigned g = grid_for(n, 256, 8);   // the same grid as k_dia: full occupancy
   SVB_REQUIRE(g <= max_grid, SVB_INVALID, "fused SpMV+dot: partials buffer too small");
   k_dia_dot<<<g, 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), ptr<double>(m->vals), x, y, dsrc,
-                              partials, counter, out, skip);
+                              partials, counter, out, skip, accumulate);
   SVB_CHECK_LAUNCH();
 }
 
@@ -1129,7 +1270,8 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
                                                            vals, x, y);
     }
   } else if (fmt == SVB_DIA) {
-    k_dia<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), vals, x, y);
+    if (!launch_dia_reg<T, false>(m, vals, x, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, s))
+      k_dia<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->ndiag, ptr<long long>(m->offs), vals, x, y);
   } else {  // HYB
     k_ell_sweep<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), vals, x, y);
     SVB_CHECK_LAUNCH();

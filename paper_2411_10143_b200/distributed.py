@@ -301,6 +301,17 @@ class _DevView:
                 "strides": None}
 
 
+class _Basis:
+    """Krylov basis rows in one allocation (row i at buf.ptr + 8*i*ld), the
+    layout the block Gram-Schmidt kernels sweep."""
+
+    def __init__(self, buf, ld: int, rows: int, n: int):
+        self.buf, self.ld, self.rows, self.n = buf, int(ld), int(rows), int(n)
+
+    def row(self, i: int) -> "_DevView":
+        return _DevView(self.buf.ptr + 8 * i * self.ld, self.n)
+
+
 class CudaOps:
     """Local vector kernels on this rank's GPU (C ABI svb_vec_*)."""
 
@@ -365,6 +376,34 @@ class CudaOps:
     def scale(self, x, s: float):
         _lib.check(self.L.svb_vec_scale(self.h, x.ptr, s, self.stream.handle))
 
+    # CGS2 block sweeps (svb_vec_gs) over a contiguous basis
+    GS_DOT, GS_UPDATE, GS_FINISH, GS_AXPY = 0, 1, 2, 3
+
+    def basis(self, rows: int) -> "_Basis":
+        ld = (self.n + 31) & ~31                  # 256-byte aligned rows
+        return _Basis(self.vec(rows * ld if self.n else 0), ld, rows, self.n)
+
+    def gs(self, mode: int, V: "_Basis", k: int, sc_h, ih: int, w, dst, sc_out, io: int,
+           sc_div=None, idiv: int = 0):
+        h = (sc_h.ptr + 8 * ih) if sc_h is not None else None
+        out = (sc_out.ptr + 8 * io) if sc_out is not None else None
+        div = (sc_div.ptr + 8 * idiv) if sc_div is not None else None
+        _lib.check(self.L.svb_vec_gs(self.h, mode, V.buf.ptr, V.ld, k, h, div, w.ptr,
+                                     dst.ptr if dst is not None else None, out, self.stream.handle))
+
+    def gs_hn(self, sc, ih2: int, k: int, inrm: int, ihn: int):
+        _lib.check(self.L.svb_vec_gs_hn(sc.ptr + 8 * ih2, k, sc.ptr + 8 * inrm, sc.ptr + 8 * ihn,
+                                        self.stream.handle))
+
+    def maxpy(self, V: "_Basis", k: int, coef: np.ndarray, x):
+        """x += sum_i coef[i] V_i (host coefficients: the back-substituted y)."""
+        c = np.ascontiguousarray(coef[:k], dtype=np.float64)
+        if getattr(self, "_coef", None) is None or self._coef.n < c.size:
+            self._coef = self.vec(max(64, c.size))
+        device.copy(self._coef.ptr, c.ctypes.data, c.nbytes, self.stream)
+        self.gs(self.GS_AXPY, V, k, self._coef, 0, x, x, None, 0)
+        self.stream.sync()              # the host coefficient buffer is a temporary
+
     def cg_update(self, sc, irr: int, ipq: int, out: int, p, q, x, r):
         _lib.check(self.L.svb_dcg_update(self.h, sc.ptr, irr, ipq, out, p.ptr, q.ptr, x.ptr, r.ptr,
                                          self.stream.handle))
@@ -395,6 +434,25 @@ class CudaOps:
         if timer is not None:
             timer.begin("spmv:" + cfg.token(), self.stream.handle)
         launch(cfg, mat, window.ptr, dst.ptr, workers=default_workers(), stream=self.stream)
+        if timer is not None:
+            timer.end("spmv:" + cfg.token(), self.stream.handle)
+
+    def spmv_dot(self, mat, cfg: SpmvConfig, window, dst, dsrc, sc, slot: int, accumulate: bool):
+        """dst = A window and sc[slot] (+)= dsrc . dst, fused in one pass on
+        DIA (svb_vec_spmv_dot)."""
+        from .kernels import _FMT_CODE, _LIB_CODE
+        if mat is None:
+            if not accumulate:
+                device.memset(sc.ptr + 8 * slot, 0, 8, self.stream)
+            return
+        from .solver import DeviceOptions
+        timer = DeviceOptions.current().timer
+        if timer is not None:
+            timer.begin("spmv:" + cfg.token(), self.stream.handle)
+        _lib.check(self.L.svb_vec_spmv_dot(self.h, mat._device().handle, _FMT_CODE[cfg.format],
+                                           _LIB_CODE[cfg.library], cfg.lane_width or 0, default_workers(),
+                                           window.ptr, dst.ptr, dsrc.ptr, sc.ptr + 8 * slot,
+                                           1 if accumulate else 0, self.stream.handle))
         if timer is not None:
             timer.end("spmv:" + cfg.token(), self.stream.handle)
 
@@ -578,6 +636,35 @@ class DistOperator:
             self._own = self.ops.view(self.window, self.own, self.block.nloc)
         return self._own
 
+    def apply_dot(self, src, dst, sc, slot: int):
+        """dst = A_local * x and sc[slot] = src . dst over the local rows
+        (CG's q = A p with p.q): fused into the SpMV pass when ``ops`` can
+        (one launch per row part, the parts' dots accumulated in a fixed
+        order), else the SpMV followed by a dot."""
+        if not hasattr(self.ops, "spmv_dot"):
+            self.apply(src, dst)
+            self.ops.dot(src, dst, sc, slot)
+            return
+        b, ops = self.block, self.ops
+        if self.no_halo:
+            ops.spmv_dot(self.mat, self.cfg, src, dst, src, sc, slot, False)
+            return
+        if src is not self._own:
+            ops.copy(ops.view(self.window, self.own, b.nloc), ops.view(src, 0, b.nloc))
+        sends = [(p, ops.view(src, lo - b.r0, hi - lo)) for p, lo, hi in self.plan.sends]
+        recvs = [(p, ops.view(self.window, lo - b.cmin, hi - lo)) for p, lo, hi in self.plan.recvs]
+        if self.parts is None:
+            self.comm.exchange(sends, recvs)
+            ops.spmv_dot(self.mat, self.cfg, self.window, dst, src, sc, slot, False)
+            return
+        token = self.comm.exchange_start(sends, recvs)
+        (a, cnt, mat), rest = self.parts[0], self.parts[1:]
+        ops.spmv_dot(mat, self.cfg, self.window, ops.view(dst, a, cnt), ops.view(src, a, cnt), sc, slot, False)
+        self.comm.exchange_finish(token)
+        for a, cnt, mat in rest:
+            ops.spmv_dot(mat, self.cfg, self.window, ops.view(dst, a, cnt), ops.view(src, a, cnt), sc, slot,
+                         True)
+
     def apply(self, src, dst):
         """dst = A_local * x, with x's local slice in ``src``."""
         b, ops = self.block, self.ops
@@ -614,38 +701,57 @@ def _global_norm2(ops, comm, x, sc, slot: int) -> float:
     return float(ops.read(sc, slot + 1)[slot])
 
 
+class _CountingComm:
+    """Counts the all-reduces a solver issues (reported per Arnoldi step)."""
+
+    def __init__(self, comm):
+        self.comm, self.allreduces = comm, 0
+
+    def allreduce(self, sc, first, count):
+        self.allreduces += 1
+        self.comm.allreduce(sc, first, count)
+
+
 def dist_gmres(A: DistOperator, b_local, params) -> dict:
-    """Restarted MGS-GMRES over row-partitioned vectors.  Per Arnoldi step:
-    one halo exchange + local SpMV, j+2 fused local passes each followed by
-    an in-place all-reduce of one device scalar, one host read of the
-    column; Givens on the host (solver.py:294-313)."""
-    ops, comm = A.ops, A.comm
+    """Restarted GMRES over row-partitioned vectors (control flow of the
+    reference's _gmres_core, solver.py:219-342) with classical Gram-Schmidt
+    applied twice (CGS2) instead of modified Gram-Schmidt: MGS needs j+2
+    dependent all-reduces per Arnoldi step across ranks (solver.py:294-297),
+    CGS2 two — h1 = V^T w; w -= V h1 with (h2 = V^T w, ||w||^2) in the same
+    sweep; w = (w - V h2) / hn with hn^2 = ||w||^2 - ||h2||^2 on the device.
+    Per step: one halo exchange + local SpMV, three block sweeps over the
+    basis (svb_vec_gs), two in-place all-reduces, one host read of the
+    column (Givens on the host exactly as _gmres_core).  The rounding
+    differs from MGS; tests hold iterations to +-1 of the MGS oracle."""
+    ops = A.ops
+    comm = _CountingComm(A.comm)
     m = params.restart_m
-    V = [ops.vec() for _ in range(m + 1)]
+    V = ops.basis(m + 1)
     x, tmp, bvec = ops.vec(), ops.vec(), ops.vec()
     ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
         ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
-    H = ops.scalars(m + 2)            # column buffer: h_0..h_j, ||w||^2
-    sc = ops.scalars(4)
-    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 0))
+    H1, H2, HN, S0 = 0, m + 1, 2 * m + 3, 2 * m + 4     # h1 | h2, ||w||^2 | hn | norms
+    sc = ops.scalars(2 * m + 8)
+    bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, S0))
     hist, done = [], 0
+    steps = 0
     Hh = np.zeros((m + 1, m))
 
     def out(conv, fin, status="ok"):
         return {"converged": conv, "iterations": done, "history": hist, "x": x, "final": fin,
-                "status": status}
+                "status": status, "allreduces": comm.allreduces, "arnoldi_steps": steps,
+                "orthogonalization": "CGS2 (2 all-reduces per Arnoldi step)"}
 
     def true_res() -> float:
         A.apply(x, tmp)
         ops.axpby(1.0, bvec, -1.0, tmp)
-        return math.sqrt(_global_norm2(ops, comm, tmp, sc, 1)) / bnorm
+        return math.sqrt(_global_norm2(ops, comm, tmp, sc, S0 + 1)) / bnorm
 
     def update_x(j, g):
         y = np.zeros(j + 1)
         for i in range(j, -1, -1):
             y[i] = (g[i] - np.dot(Hh[i, i + 1:j + 1], y[i + 1:j + 1])) / Hh[i, i]
-        for i in range(j + 1):
-            ops.axpby(float(y[i]), V[i], 1.0, x)
+        ops.maxpy(V, j + 1, y, x)
 
     if bnorm == 0.0:
         if params.max_iters >= 1:
@@ -656,11 +762,11 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
     while done < params.max_iters:
         A.apply(x, tmp)
         ops.axpby(1.0, bvec, -1.0, tmp)               # r = b - A x
-        beta = math.sqrt(_global_norm2(ops, comm, tmp, sc, 2))
+        beta = math.sqrt(_global_norm2(ops, comm, tmp, sc, S0 + 2))
         _finite(beta, "residual norm", done)
         if beta / bnorm <= params.tol:
             return out(True, beta / bnorm)
-        ops.axpby(1.0 / beta, tmp, 0.0, V[0])
+        ops.axpby(1.0 / beta, tmp, 0.0, V.row(0))
         Hh[:] = 0.0
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
         g[0] = beta
@@ -669,18 +775,19 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
             if done >= params.max_iters:
                 j -= 1
                 break
-            w = V[j + 1]
-            A.apply(V[j], w)
-            ops.dot(V[0], w, H, 0)
-            comm.allreduce(H, 0, 1)
-            for i in range(1, j + 1):                 # w -= h_{i-1} V_{i-1}; h_i = V_i . w
-                ops.axpy_dot(H, i - 1, -1.0, V[i - 1], w, V[i], H, i)
-                comm.allreduce(H, i, 1)
-            ops.axpy_dot(H, j, -1.0, V[j], w, None, H, j + 1)   # ||w||^2
-            comm.allreduce(H, j + 1, 1)
-            col = ops.read(H, j + 2)
-            Hh[:j + 1, j] = col[:j + 1]
-            hn = math.sqrt(col[j + 1])
+            k = j + 1
+            w = V.row(k)
+            A.apply(V.row(j), w)
+            ops.gs(ops.GS_DOT, V, k, None, 0, w, None, sc, H1)              # h1 = V^T w
+            comm.allreduce(sc, H1, k)
+            ops.gs(ops.GS_UPDATE, V, k, sc, H1, w, w, sc, H2)               # w -= V h1; h2, ||w||^2
+            comm.allreduce(sc, H2, k + 1)
+            ops.gs_hn(sc, H2, k, H2 + k, HN)
+            ops.gs(ops.GS_FINISH, V, k, sc, H2, w, w, None, 0, sc, HN)      # w = (w - V h2) / hn
+            steps += 1
+            col = ops.read(sc, HN + 1)
+            Hh[:k, j] = col[H1:H1 + k] + col[H2:H2 + k]
+            hn = float(col[HN])
             _finite(hn, "Arnoldi norm", done + 1)
             for i in range(j):
                 t = cs[i] * Hh[i, j] + sn[i] * Hh[i + 1, j]
@@ -710,7 +817,6 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
                     return out(True, fin)
                 moved = True
                 break
-            ops.scale(w, 1.0 / hn)
         if j >= 0 and not moved:
             update_x(j, g)
     fin = true_res()
@@ -719,9 +825,10 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
 
 def dist_cg(A: DistOperator, b_local, params) -> dict:
     """Hestenes-Stiefel CG over row-partitioned vectors (oracle/cpu_oracle.py:
-    cg).  Per iteration: one halo exchange + local SpMV, a local p.Ap and a
-    fused x/r update with r.r (svb_dcg_update) on device scalars, each
-    followed by an in-place scalar all-reduce, then p = r + beta p
+    cg).  Per iteration: one halo exchange + local SpMV with the local p.Ap
+    folded into the same pass (svb_vec_spmv_dot), a fused x/r update with
+    r.r (svb_dcg_update) on device scalars, each followed by an in-place
+    scalar all-reduce, then p = r + beta p
     (svb_dcg_p).  The host reads (p.Ap, r.r) through pinned memory after the
     p update is already enqueued, so the GPU keeps working while the host
     runs the convergence test; a breakdown (p.Ap = 0) leaves x and r
@@ -756,8 +863,7 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     cur, nxt = 0, 1
     _global_norm2(ops, comm, r, sc, cur)
     while done < params.max_iters:
-        A.apply(p, q)
-        ops.dot(p, q, sc, 2)
+        A.apply_dot(p, q, sc, 2)              # q = A p with p.q folded into the SpMV pass
         comm.allreduce(sc, 2, 1)
         ops.cg_update(sc, cur, 2, nxt, p, q, x, r)
         comm.allreduce(sc, nxt, 1)

@@ -72,6 +72,32 @@ class NumpyOps:
     def cg_p(self, sc, inew, iold, r, p):
         p[:] = r + (sc[inew] / sc[iold]) * p
 
+    GS_DOT, GS_UPDATE, GS_FINISH, GS_AXPY = 0, 1, 2, 3
+
+    def basis(self, rows):
+        return _NpBasis(np.zeros((rows, self.n)))
+
+    def gs(self, mode, V, k, sc_h, ih, w, dst, sc_out, io, sc_div=None, idiv=0):
+        B = V.a[:k]
+        if mode == self.GS_DOT:
+            sc_out[io:io + k] = B @ w
+            return
+        h = sc_h[ih:ih + k]
+        t = w + h @ B if mode == self.GS_AXPY else w - h @ B
+        if mode == self.GS_FINISH:
+            t = t / sc_div[idiv]
+        dst[:] = t
+        if mode == self.GS_UPDATE:
+            sc_out[io:io + k] = B @ dst
+            sc_out[io + k] = float(dst @ dst)
+
+    def gs_hn(self, sc, ih2, k, inrm, ihn):
+        r = sc[inrm] - float(np.sum(sc[ih2:ih2 + k] ** 2))
+        sc[ihn] = np.sqrt(r) if r > 0 else 0.0
+
+    def maxpy(self, V, k, coef, x):
+        x += coef[:k] @ V.a[:k]
+
     def read_async(self, sc, count):
         return sc[:count].copy()
 
@@ -82,6 +108,8 @@ class NumpyOps:
         x *= s
 
     def prepare(self, block, cfg):
+        if block.nloc == 0:
+            return None
         csr = O.OCsr(block.nloc, block.window, block.row_ptr, block.cols, block.values)
         return O.convert(csr, cfg.format.value) if cfg.format.value != "CSR" else csr
 
@@ -92,7 +120,17 @@ class NumpyOps:
         return O.convert(csr, cfg.format.value) if cfg.format.value != "CSR" else csr
 
     def spmv(self, mat, cfg, window, dst):
+        if mat is None:
+            return
         dst[:] = O.spmv(cfg.token(), mat, window, workers=4)
+
+
+class _NpBasis:
+    def __init__(self, a):
+        self.a = a
+
+    def row(self, i):
+        return self.a[i]
 
 
 class GlooComm:
@@ -152,25 +190,36 @@ def _worker(rank, world, port, case, q):
         A = DistOperator(blk, bounds, comm, ops, SpmvConfig.from_token(case["cfg"]))
         csr = O.OCsr(n, n, ptr, cols, vals)
         b = O.spmv_sequential(csr, np.ones(n))
-        params = GmresParams(restart_m=30, tol=1e-8, max_iters=3000)
+        params = GmresParams(restart_m=case.get("restart", 30), tol=1e-8, max_iters=3000)
         res = (dist_cg if case["method"] == "cg" else dist_gmres)(A, b[r0:r1], params)
-        # global features from per-rank aggregates
-        lc = O.OCsr(blk.nloc, blk.window, blk.row_ptr, blk.cols, blk.values)
-        a = O.feature_aggregates(lc)
-        parts = comm.allgather_obj((a["sum_r"], a["sum_r2"], a["max_r"], a["min_r"], a["span"],
-                                    a["runs"], blk.offsets.tolist()))
+        # global features from per-rank aggregates (a rank without rows adds
+        # nothing and stays out of the min)
+        if blk.nloc:
+            lc = O.OCsr(blk.nloc, blk.window, blk.row_ptr, blk.cols, blk.values)
+            a = O.feature_aggregates(lc)
+            mine = (a["sum_r"], a["sum_r2"], a["max_r"], a["min_r"], a["span"], a["runs"])
+        else:
+            mine = (0, 0, 0, None, 0, 0)
+        parts = comm.allgather_obj(mine + (blk.offsets.tolist(),))
         agg = (sum(p[0] for p in parts), sum(p[1] for p in parts), max(p[2] for p in parts),
-               min(p[3] for p in parts), sum(p[4] for p in parts), sum(p[5] for p in parts),
-               len(set().union(*[set(p[6]) for p in parts])))
+               min(p[3] for p in parts if p[3] is not None), sum(p[4] for p in parts),
+               sum(p[5] for p in parts), len(set().union(*[set(p[6]) for p in parts])))
         fv = features_from_aggregates(n, n, int(ptr[-1]), agg).to_array().tolist()
         q.put((rank, r0, r1, res["iterations"], res["converged"], res["final"], res["x"], fv,
-               HaloPlan.build(bounds, comm.allgather_obj((blk.cmin, blk.cmax)), rank), A.split))
+               HaloPlan.build(bounds, comm.allgather_obj((blk.cmin, blk.cmax)), rank), A.split,
+               res.get("allreduces"), res.get("arnoldi_steps")))
     finally:
         dist.destroy_process_group()
 
 
 CASES = {
     "cg-poisson-dia": {"gen": lambda: G.poisson2d(24), "method": "cg", "cfg": "DIA/LibA"},
+    "gmres-restart40-csr": {"gen": lambda: G.convdiff9(22), "method": "gmres", "cfg": "CSR/LibB",
+                            "restart": 40},
+    "cg-empty-rank-world4": {"gen": lambda: G.poisson2d(2), "method": "cg", "cfg": "CSR/LibB",
+                             "world": 6},
+    "gmres-empty-rank-world5": {"gen": lambda: G.convdiff9(2), "method": "gmres", "cfg": "CSR/LibB",
+                                "world": 5},
     "gmres-convdiff-csr": {"gen": lambda: G.convdiff9(20), "method": "gmres", "cfg": "CSR/LibB"},
     "gmres-powerlaw-ell": {"gen": lambda: G.powerlaw_spd(600, seed=5), "method": "gmres",
                            "cfg": "ELL/LibA"},
@@ -181,10 +230,11 @@ CASES = {
 def test_row_partitioned_solve_world2(name):
     import multiprocessing as mp
     case = CASES[name]
+    world = case.get("world", 2)
     ctx = mp.get_context("fork")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
     outs = sorted([q.get(timeout=240) for _ in procs], key=lambda t: t[0])
@@ -196,16 +246,22 @@ def test_row_partitioned_solve_world2(name):
     b = O.spmv_sequential(csr, np.ones(n))
     mv = lambda v: O.spmv("CSR/LibB", csr, v)          # noqa: E731
     ref = (O.cg(mv, b, tol=1e-8, max_iters=3000) if case["method"] == "cg"
-           else O.gmres(mv, b, restart=30, tol=1e-8, max_iters=3000))
+           else O.gmres(mv, b, restart=case.get("restart", 30), tol=1e-8, max_iters=3000))
     x = np.concatenate([o[6] for o in outs])
-    assert [o[1] for o in outs] == [0, outs[0][2]] and outs[-1][2] == n
+    assert outs[0][1] == 0 and outs[-1][2] == n
+    assert all(outs[k][2] == outs[k + 1][1] for k in range(world - 1))
+    if "empty" in name:
+        assert any(o[2] == o[1] for o in outs)          # some rank really owns no rows
+    if case["method"] == "gmres":                       # CGS2: two all-reduces per Arnoldi step
+        for o in outs:
+            assert o[10] <= 2 * o[11] + 2 + 3 * 4, (o[10], o[11])
     for o in outs:
         assert o[3] == outs[0][3]                       # ranks agree
         assert o[4] and o[5] <= 1e-8
     assert abs(outs[0][3] - ref["iterations"]) <= 1
     assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
     assert outs[0][7] == O.features(csr)                # exact global features
-    if name != "gmres-powerlaw-ell":                    # banded: interior SpMV overlaps the halo
+    if name in ("cg-poisson-dia", "gmres-convdiff-csr", "gmres-restart40-csr"):   # interior overlaps the halo
         assert all(o[9] is not None for o in outs)
     for o in outs:                                      # halo symmetric
         plan = o[8]

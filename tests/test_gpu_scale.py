@@ -170,15 +170,24 @@ def test_config1_cg_matches_oracle_iterations():
         assert rep.final_residual <= 1e-8
 
 
-def test_config3_cg_matches_oracle_iterations():
+def test_config3_cg_within_the_references_own_spread():
+    """Config 3 is ill-conditioned (~300 CG iterations): the iteration count
+    moves with the summation order of the inner products alone — the
+    reference's np.dot order depends on the CPU's BLAS kernel and thread
+    count.  tests/golden/make_cg_spread.py reran the oracle CG (bit-exact
+    reference matvec) with four valid fp64 inner-product orders; the CUDA CG
+    (device tree reductions) must land within that spread +-1."""
     c = fixtures()["config3"]["cg"]
+    spread = fixtures()["config3"].get("cg_spread", {"min": c["iterations"], "max": c["iterations"]})
+    lo, hi = spread["min"] - 1, spread["max"] + 1
     A = matrix("config3")
     params = P.GmresParams(tol=1e-8, max_iters=20000, rhs="random", seed=0)
     for rep in (P.cg_solve(A, None, params, initial_config=P.SpmvConfig.from_token(c["matvec"])),
                 P.async_solve(A, None, params, P.CascadeModelSet.load_dir(MODELS), method="cg",
                               initial_config=P.GPU_DEFAULT_CONFIG)):
-        assert rep.converged and abs(rep.iterations - c["iterations"]) <= 1
+        assert rep.converged and lo <= rep.iterations <= hi, (rep.iterations, spread)
         assert rep.final_residual <= 1e-8
+        assert np.allclose(rep.residual_history[:5], c["history_head"], rtol=1e-9, atol=0)
 
 
 def test_int64_row_pointers_on_the_golden_cases():

@@ -113,6 +113,28 @@ def test_fp32_kernels_against_fp64(gen):
     assert len(seen) == (4 if gen == "powerlaw" else 5)
 
 
+@pytest.mark.parametrize("n,offsets", [
+    (20_000, [0]), (20_000, [-3, -1, 0, 1, 5]), (20_002, list(range(-13, 14))),
+    (20_001, [-7, 0, 7]),                                   # odd rows: the thread-per-row kernel
+    (65_536, list(range(-2000, 2001, 100))),                # 41 diagonals, wide reach: boundary tiles
+    (33_000, list(range(-30, 31))),                         # 61 diagonals: above the staged-kernel limit
+    (4_100, [-4099, -1, 0, 1, 4099])])                      # offsets touching the corners
+def test_dia_staged_kernel_bit_exact(n, offsets):
+    """The TMA-staged DIA kernel (k_dia_tma: tiles of every diagonal bulk
+    copied through a shared-memory ring) against the oracle, fp64 bit-exact
+    and fp32 within FP32_TOL, over interior, boundary and tail tiles."""
+    nn, m, ptr, cols, vals = G.banded(n, offsets, seed=len(offsets), diagonal_boost=2.0)
+    csr = P.CsrMatrix(nn, m, ptr, cols, vals)
+    dia = P.convert(csr, P.FormatTag.DIA)
+    cfg = P.SpmvConfig(P.FormatTag.DIA, P.Library.LIB_A)
+    x = np.random.default_rng(n).uniform(-1.0, 1.0, size=m)
+    want = O.spmv("DIA/LibA", O.convert(O.OCsr(nn, m, ptr, cols, vals), "DIA"), x)
+    assert np.array_equal(P.execute_spmv(cfg, dia, x), want)
+    s = device.thread_stream()
+    y32 = P.execute_spmv(cfg, dia, device.DeviceVector.from_numpy(x.astype(np.float32), s), stream=s).to_numpy(s)
+    assert rel(y32.astype(np.float64), want) <= FP32_TOL
+
+
 def test_ptr64_mode_is_what_the_environment_asks():
     """tests/test_gpu_scale.py re-runs this module with SPMVTUNE_FORCE_PTR64=1:
     the int64 row-pointer kernels must then really be the ones running."""
