@@ -225,6 +225,21 @@ int svb_spmv_sequential(const svb_matrix* csr, const double* x_dev, double* y_de
  * ndiag}; the host evaluates the 15 float features with the reference's own
  * expressions (features.py:103-110, 147-150), making them bit-exact. */
 int svb_features(const svb_matrix* csr, int64_t* agg_host, void* stream);
+/* The same pass as a job, for extract_features(csr, cancel, counter=...)
+ * (features.py:68-156): start enqueues it on `stream` and returns at once;
+ * cancel raises a host-mapped flag the kernel polls once per 256-row tile
+ * (it then stops reading row_ptr/col_idx; the reference checks every
+ * row_chunk rows, features.py:89-91); query reports completion without
+ * blocking; finish waits, writes agg[7], counters[2] = {row_ptr elements,
+ * col_idx elements} actually read (TraversalCounter, features.py:60-65) and
+ * *cancelled, and releases the job.  precancelled != 0 reads nothing.  An
+ * uncancelled pass leaves its diagonal bitmap and sorted offsets on the
+ * handle for a later DIA conversion. */
+typedef struct svb_features_job svb_features_job;
+int svb_features_start(const svb_matrix* csr, int precancelled, void* stream, svb_features_job** job);
+int svb_features_cancel(svb_features_job* job);
+int svb_features_query(svb_features_job* job, int* done);
+int svb_features_finish(svb_features_job* job, int64_t* agg_host, int64_t* counters_host, int* cancelled);
 /* The distinct diagonal offsets (col - row) of a CSR handle plus `shift`,
  * ascending (the ndiag feature's set, features.py:118-126; a row-partitioned
  * rank passes shift = cmin - r0 for global offsets so the ranks' sets can be

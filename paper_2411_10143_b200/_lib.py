@@ -128,6 +128,10 @@ _SIGS = {
     "svb_spmv_host": [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P],
     "svb_spmv_sequential": [_P, _P, _P, _P],
     "svb_features": [_P, _PI64, _P],
+    "svb_features_start": [_P, C.c_int, _P, _PP],
+    "svb_features_cancel": [_P],
+    "svb_features_query": [_P, C.POINTER(C.c_int32)],
+    "svb_features_finish": [_P, _PI64, _PI64, C.POINTER(C.c_int32)],
     "svb_krylov_create": [_I64, _I32, _PP],
     "svb_krylov_destroy": [_P],
     "svb_krylov_vec": [_P, C.c_int, _PP],

@@ -426,13 +426,60 @@ static svb_matrix* build_ell(const RowView& v, int64_t max_cells, cudaStream_t s
   return m;
 }
 
+// DiaMatrix keeps no nnz; report the stored (in-range) cells like svb_dia_create
+static int64_t dia_stored(const std::vector<int64_t>& offs, int64_t nrows, int64_t ncols) {
+  int64_t stored = 0;
+  for (const int64_t off : offs) {
+    const int64_t lo = off < 0 ? -off : 0, hi = std::min<int64_t>(nrows, ncols - off);
+    if (hi > lo) stored += hi - lo;
+  }
+  return stored;
+}
+
+// DIA data from the row view, every cell written once (m->offs on device)
+static void fill_dia(const RowView& v, svb_matrix* m, cudaStream_t s) {
+  const size_t dsm = (size_t)DIA_TILE_CAP * 12 + (size_t)m->ndiag * 8;
+  static const bool attr = [] {   // once per process (thread-safe static init)
+    SVB_CUDA_TRY(cudaFuncSetAttribute(k_csr_to_dia, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)DIA_TILE_CAP * 12 + (size_t)DIA_CAP * 8)));
+    return true;
+  }();
+  (void)attr;
+  k_csr_to_dia<<<grid_for(v.nrows, TILE_ROWS, 4), TILE_ROWS, dsm, s>>>(v.nrows, m->ndiag, ptr<long long>(m->offs),
+                                                                     ptr<int64_t>(v.ptr), ptr<int>(v.cols),
+                                                                     ptr<double>(v.vals), ptr<double>(m->vals));
+  SVB_CHECK_LAUNCH();
+}
+
 static svb_matrix* build_dia(const RowView& v, const svb_matrix* src, cudaStream_t s) {
   const int64_t nbits = v.nrows + v.ncols - 1;
   const int64_t nwords = (nbits + 31) / 32;
   Buf bits;
+  std::vector<int64_t> cached;   // sorted offsets the feature pass left on the CSR handle
+  bool have_offs = false;
   if (src->fmt == SVB_CSR) {   // the bitmap feature extraction left on the handle
     std::lock_guard<std::mutex> lk(src->mu);
-    if (src->diag_bits && src->diag_bits->bytes >= (size_t)nwords * 4) bits = src->diag_bits;
+    if (src->diag_bits && src->diag_bits->bytes >= (size_t)nwords * 4) {
+      bits = src->diag_bits;
+      if (src->diag_offs_valid) {
+        cached = src->diag_offs;
+        have_offs = true;
+      }
+    }
+  }
+  if (have_offs) {
+    const int64_t ndiag = (int64_t)cached.size();
+    auto m = new_like(v, SVB_DIA);
+    m->ndiag = ndiag;
+    m->offs = alloc(ndiag * 8, s);
+    m->vals = alloc(ndiag * v.nrows * 8, s);
+    m->h_offs = cached;
+    if (ndiag) {
+      SVB_CUDA_TRY(cudaMemcpyAsync(m->offs->ptr, m->h_offs.data(), ndiag * 8, cudaMemcpyHostToDevice, s));
+      fill_dia(v, m, s);
+    }
+    m->nnz = dia_stored(m->h_offs, v.nrows, v.ncols);
+    return m;
   }
   const bool reused = (bool)bits;
   if (!reused) {
@@ -461,29 +508,12 @@ static svb_matrix* build_dia(const RowView& v, const svb_matrix* src, cudaStream
     k_bits_to_offsets<<<grid_for(nwords, 256), 256, 0, s>>>(nwords, v.nrows, ptr<unsigned>(bits),
                                                             ptr<int64_t>(pos), ptr<long long>(m->offs));
     SVB_CHECK_LAUNCH();
-    const size_t dsm = (size_t)DIA_TILE_CAP * 12 + (size_t)ndiag * 8;
-    static const bool attr = [] {   // once per process (thread-safe static init)
-      SVB_CUDA_TRY(cudaFuncSetAttribute(k_csr_to_dia, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)((size_t)DIA_TILE_CAP * 12 + (size_t)DIA_CAP * 8)));
-      return true;
-    }();
-    (void)attr;
-    k_csr_to_dia<<<grid_for(v.nrows, TILE_ROWS, 4), TILE_ROWS, dsm, s>>>(v.nrows, ndiag, ptr<long long>(m->offs),
-                                                                   ptr<int64_t>(v.ptr), ptr<int>(v.cols),
-                                                                   ptr<double>(v.vals), ptr<double>(m->vals));
-    SVB_CHECK_LAUNCH();
+    fill_dia(v, m, s);
     m->h_offs.resize(ndiag);
     SVB_CUDA_TRY(cudaMemcpyAsync(m->h_offs.data(), m->offs->ptr, ndiag * 8, cudaMemcpyDeviceToHost, s));
+    SVB_CUDA_TRY(cudaStreamSynchronize(s));
   }
-  // DiaMatrix keeps no nnz; report the stored (in-range) cells like svb_dia_create
-  int64_t stored = 0;
-  SVB_CUDA_TRY(cudaStreamSynchronize(s));
-  for (int64_t k = 0; k < ndiag; ++k) {
-    const int64_t off = m->h_offs[k];
-    const int64_t lo = off < 0 ? -off : 0, hi = std::min<int64_t>(v.nrows, v.ncols - off);
-    if (hi > lo) stored += hi - lo;
-  }
-  m->nnz = stored;
+  m->nnz = dia_stored(m->h_offs, v.nrows, v.ncols);
   return m;
 }
 

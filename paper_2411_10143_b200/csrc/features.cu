@@ -9,6 +9,10 @@
 // evaluates the floats with the reference's own expressions, so the feature
 // vector is bit-identical to the CPU path.
 #include <algorithm>
+#include <climits>
+#include <cstddef>
+#include <mutex>
+#include <vector>
 
 #include "matrix.cuh"
 
@@ -95,32 +99,99 @@ __device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e
   *span_out = (long long)last - first;
 }
 
-template <class P, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __restrict__ ptr,
-                                                    const int* __restrict__ cols,
-                                                    unsigned* __restrict__ bits, FeatAcc* out) {
-  constexpr int CAP = 8192;  // staged column indices per tile (32 KB)
-  __shared__ int scol[CAP];
+// One pass over row_ptr and col_idx through the row-tile ring (matrix.cuh):
+// one thread per row walks its staged columns (run lengths, span, diagonal
+// marks); rows longer than FEAT_LONG go to a warp.  Thread 0 polls the
+// cancel flag one tile ahead and, once it is raised, stops refilling the
+// ring; the tiles already in flight are drained without being walked.  The
+// flag is a device word (an L2 read per tile): svb_features_cancel raises it
+// with a 4-byte copy on a side stream, which the copy engine performs while
+// the kernel runs.  (Polling host-mapped memory instead costs a PCIe round
+// trip per tile, and those reads serialise: 12 ms for a 4 M-row pass.)  Rows and entries actually
+// walked are counted (the reference's TraversalCounter, features.py:60-65).
+constexpr int FEAT_R = 256, FEAT_CAP = 3072, FEAT_NS = 3;
+
+struct FeatOut {
+  FeatAcc a;
+  unsigned long long ndiag;                  // popcount of the bitmap
+  unsigned long long rows_read, cols_read;   // row_ptr / col_idx elements consumed
+  unsigned long long noffs;                  // offsets written below (may exceed the cap)
+  int cancelled;
+  int pad;
+  long long offs[4096];                      // diagonal offsets (unordered) when ndiag <= 4096
+};
+
+template <class P>
+__global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __restrict__ ptr,
+                                                     const int* __restrict__ cols, unsigned* __restrict__ bits,
+                                                     FeatOut* out, const volatile int* cancel) {
+  using Lay = RingLayout<P, FEAT_R, FEAT_CAP, false>;
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ alignas(8) uint64_t bar[FEAT_NS];
+  __shared__ RingDesc desc[FEAT_NS];
   __shared__ long long dcache[DIAG_CACHE];
-  __shared__ int lrows[BLOCK];
-  __shared__ int nl;
-  diag_cache_init(dcache);   // (the tile loop's first __syncthreads orders it)
-  if (threadIdx.x == 0) nl = 0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int lrows[FEAT_R];
+  __shared__ int nlong[2], sstop;   // long-row count, double-buffered by iteration parity
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  diag_cache_init(dcache);
+  const int64_t ntiles = (nrows + FEAT_R - 1) / FEAT_R;
+  const uint64_t policy = l2_evict_first_policy();
+  int cflag = 0;   // thread 0: the cancel flag as read one tile ago
+  auto issue = [&](int st, int64_t tile, int64_t e0, int64_t e1) {
+    const int64_t r0 = tile * FEAT_R, r1 = min(r0 + FEAT_R, nrows);
+    ring_issue<P, FEAT_R, FEAT_CAP, false>(ring + st * Lay::STAGE, &bar[st], &desc[st], r0, r1, e0, e1, ptr, cols,
+                                          nullptr, policy);
+  };
+  auto bounds_of = [&](int64_t tile, int64_t& e0, int64_t& e1) {
+    e0 = (int64_t)ptr[tile * FEAT_R];
+    e1 = (int64_t)ptr[min(tile * FEAT_R + FEAT_R, nrows)];
+  };
+  if (tid == 0) {
+    nlong[0] = nlong[1] = 0;
+    sstop = 0;
+    for (int st = 0; st < FEAT_NS; ++st) mbar_init(&bar[st], 1);
+    if (cancel) cflag = *cancel;
+    for (int st = 0; st < FEAT_NS; ++st) {
+      const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+      if (tile < ntiles && !cflag) {
+        int64_t e0, e1;
+        bounds_of(tile, e0, e1);
+        issue(st, tile, e0, e1);
+      }
+    }
+    if (cflag) sstop = 1;
+  }
+  __syncthreads();
   FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
-  const int64_t ntiles = (nrows + BLOCK - 1) / BLOCK;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const StagedRows<P> t = stage_row_tile<P, BLOCK, CAP>(tile, nrows, ptr, cols, scol);
-    auto col = [&](int64_t k) { return t.staged ? scol[k] : __ldg(cols + t.base + k); };
-    const int64_t i = t.r0 + threadIdx.x;
-    if (i < t.r1) {
-      const int64_t s = (int64_t)ptr[i] - t.base, e = (int64_t)ptr[i + 1] - t.base, L = e - s;
+  unsigned long long rows_read = 0, cols_read = 0;
+  int64_t stop_at = sstop ? -1 : INT64_MAX;   // first iteration whose tile was not issued
+  for (int64_t tile = blockIdx.x, it = 0; tile < ntiles && it < stop_at; tile += gridDim.x, ++it) {
+    const int st = (int)(it % FEAT_NS);
+    int& nl = nlong[it & 1];
+    int nxt_cancel = 0;
+    const int64_t tn = tile + (int64_t)FEAT_NS * gridDim.x;   // the tile this stage takes next
+    int64_t ne0 = 0, ne1 = 0;
+    if (tid == 0) {
+      nlong[(it + 1) & 1] = 0;   // last read before the previous iteration's final barrier
+      if (cancel) nxt_cancel = *cancel;   // consumed after this tile (latency hidden)
+      if (tn < ntiles) bounds_of(tn, ne0, ne1);   // likewise: used by the refill below
+    }
+    mbar_wait(&bar[st], (uint32_t)(it / FEAT_NS) & 1u);
+    const RingDesc d = desc[st];
+    const bool walk = stop_at == INT64_MAX;
+    const unsigned char* stage = ring + st * Lay::STAGE;
+    const int* scol = reinterpret_cast<const int*>(stage + Lay::SV) + d.coff;
+    const P* sp = reinterpret_cast<const P*>(stage + Lay::SV + Lay::SC) + d.poff;
+    auto col = [&](int64_t k) { return d.staged ? scol[k] : __ldg(cols + d.e0 + k); };
+    const int64_t i = d.r0 + tid;
+    if (walk && i < d.r1) {
+      const int64_t s = (int64_t)sp[tid] - d.e0, e = (int64_t)sp[tid + 1] - d.e0, L = e - s;
       a.sum_r += (unsigned long long)L;
       a.sum_r2 += (unsigned long long)(L * L);
       a.max_r = max(a.max_r, (long long)L);
       a.min_r = min(a.min_r, (long long)L);
       if (L > FEAT_LONG) {
-        lrows[atomicAdd(&nl, 1)] = threadIdx.x;
+        lrows[atomicAdd(&nl, 1)] = tid;
       } else if (L > 0) {
         const int64_t diag0 = nrows - 1 - i;
         const int c0 = col(s);
@@ -138,10 +209,14 @@ __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __re
         a.runs += (unsigned long long)best;
       }
     }
+    if (walk && tid == 0) {
+      rows_read += (unsigned long long)(d.r1 - d.r0 + 1);
+      cols_read += (unsigned long long)(d.e1 - d.e0);
+    }
     __syncthreads();
-    for (int q = warp; q < nl; q += BLOCK / 32) {
-      const int64_t r = t.r0 + lrows[q];
-      const int64_t s = (int64_t)ptr[r] - t.base, e = (int64_t)ptr[r + 1] - t.base;
+    for (int q = warp; q < nl; q += FEAT_R / 32) {
+      const int64_t r = d.r0 + lrows[q];
+      const int64_t s = (int64_t)sp[lrows[q]] - d.e0, e = (int64_t)sp[lrows[q] + 1] - d.e0;
       long long best, span;
       warp_row_runs(col, s, e, nrows - 1 - r, bits, dcache, &best, &span);
       if (lane == 0) {
@@ -149,10 +224,25 @@ __global__ void __launch_bounds__(BLOCK) k_features(int64_t nrows, const P* __re
         a.runs += (unsigned long long)best;
       }
     }
-    __syncthreads();   // every warp is done with nl / lrows
-    if (threadIdx.x == 0) nl = 0;
+    if (tid == 0) {
+      if (cflag) sstop = 1;   // raised one tile ago: stop refilling from here
+      cflag = nxt_cancel;
+    }
+    __syncthreads();   // stage st, nl/lrows and sstop settled
+    if (sstop && stop_at == INT64_MAX) stop_at = it + FEAT_NS;   // drain what is in flight
+    if (tid == 0) {
+      if (!sstop && tn < ntiles) {
+        fence_proxy_async_smem();
+        issue(st, tn, ne0, ne1);
+      }
+    }
   }
-  block_reduce_store<BLOCK>(a, out);
+  block_reduce_store<FEAT_R>(a, &out->a);
+  if (tid == 0) {
+    if (rows_read) atomicAdd(&out->rows_read, rows_read);
+    if (cols_read) atomicAdd(&out->cols_read, cols_read);
+    if (sstop) atomicExch(&out->cancelled, 1);
+  }
 }
 
 __global__ void k_popcount(int64_t nwords, const unsigned* __restrict__ bits,
@@ -174,8 +264,15 @@ __global__ void k_popcount(int64_t nwords, const unsigned* __restrict__ bits,
 
 // set bits of the diagonal bitmap -> offsets (bit - (nrows - 1) + shift),
 // unordered (the host sorts them)
+// (skip_above: the popcount; above the cap the list is not wanted and the
+// counter atomics of millions of set words would be pure contention)
 __global__ void k_bits_to_offsets(int64_t nwords, const unsigned* __restrict__ bits, int64_t base,
-                                  long long* __restrict__ out, int64_t cap, unsigned long long* __restrict__ cnt) {
+                                  long long* __restrict__ out, int64_t cap, unsigned long long* __restrict__ cnt,
+                                  const unsigned long long* __restrict__ skip_above = nullptr) {
+  if (skip_above && *skip_above > (unsigned long long)cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = *skip_above;
+    return;
+  }
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
        w += (int64_t)gridDim.x * blockDim.x) {
     unsigned b = bits[w];
@@ -194,50 +291,213 @@ __global__ void k_bits_to_offsets(int64_t nwords, const unsigned* __restrict__ b
 
 using namespace svb;
 
-extern "C" int svb_features(const svb_matrix* m, int64_t* agg, void* stream) {
+// ---------------------------------------------------------------------------
+// Feature jobs: the pass is enqueued (svb_features_start) and its result
+// block (aggregates, traversal counters, cancel outcome and the diagonal
+// offsets) lands in pinned host memory behind an event, so the caller never
+// blocks inside the library while the pass runs: it polls, may raise the
+// cancel flag (a device word the kernel reads one tile ahead), and
+// collects the result with svb_features_finish.  A completed, uncancelled
+// pass leaves its diagonal bitmap and sorted offsets on the CSR handle for
+// a later DIA conversion (no second pass over col_idx, no offset scan).
+// ---------------------------------------------------------------------------
+struct svb_features_job {
+  const svb_matrix* m = nullptr;
+  cudaStream_t s = nullptr;
+  FeatOut* host = nullptr;     // pinned result block
+  int* flag = nullptr;         // device cancel word; 0 whenever the job is idle
+  cudaEvent_t done = nullptr;
+  bool cancel_requested = false;
+  Buf bits, out;
+};
+
+namespace {
+std::mutex g_job_mu;
+std::vector<svb_features_job*> g_job_pool;   // pinned blocks are slow to allocate: recycle jobs
+
+// the side stream and the pinned source word of cancel requests
+struct CancelPath {
+  cudaStream_t s = nullptr;
+  int* one = nullptr;
+  CancelPath() {
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaHostAlloc((void**)&one, sizeof(int), cudaHostAllocDefault) != cudaSuccess)
+      throw Error{SVB_CUDA, "cannot create the feature-cancel stream"};
+    *one = 1;
+  }
+};
+CancelPath& cancel_path() {
+  static CancelPath p;
+  return p;
+}
+
+svb_features_job* job_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_job_mu);
+    if (!g_job_pool.empty()) {
+      auto* j = g_job_pool.back();
+      g_job_pool.pop_back();
+      return j;
+    }
+  }
+  auto* j = new svb_features_job();
+  try {
+    SVB_CUDA_TRY(cudaHostAlloc((void**)&j->host, sizeof(FeatOut), cudaHostAllocDefault));
+    SVB_CUDA_TRY(cudaMalloc((void**)&j->flag, 16));
+    SVB_CUDA_TRY(cudaMemset(j->flag, 0, 16));
+    SVB_CUDA_TRY(cudaEventCreateWithFlags(&j->done, cudaEventDisableTiming));
+  } catch (...) {
+    if (j->host) cudaFreeHost(j->host);
+    if (j->flag) cudaFree(j->flag);
+    delete j;
+    throw;
+  }
+  return j;
+}
+
+void job_put(svb_features_job* j) {
+  j->bits.reset();
+  j->out.reset();
+  j->m = nullptr;
+  j->cancel_requested = false;
+  std::lock_guard<std::mutex> lk(g_job_mu);
+  g_job_pool.push_back(j);
+}
+}  // namespace
+
+extern "C" int svb_features_start(const svb_matrix* m, int precancelled, void* stream, svb_features_job** job) {
   return guard([&] {
-    SVB_REQUIRE(m && agg, SVB_INVALID, "null handle");
+    SVB_REQUIRE(m && job, SVB_INVALID, "null handle");
     SVB_REQUIRE(m->fmt == SVB_CSR, SVB_UNSUPPORTED_CONFIG, "extract_features expects CSR");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int64_t nbits = m->nrows + m->ncols - 1;
-    const int64_t nwords = (nbits + 31) / 32;
-    Buf bits = alloc(nwords * 4, s);
-    Buf acc = alloc(sizeof(FeatAcc) + 8, s);
-    SVB_CUDA_TRY(cudaMemsetAsync(bits->ptr, 0, nwords * 4, s));
-    FeatAcc init{0, 0, 0, 0, 0, LLONG_MAX};
-    SVB_CUDA_TRY(cudaMemcpyAsync(acc->ptr, &init, sizeof(FeatAcc), cudaMemcpyHostToDevice, s));
-    SVB_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(acc->ptr) + sizeof(FeatAcc), 0, 8, s));
-    constexpr int B = 256;
-    const unsigned g = grid_for(m->nrows, B, 8);
-    if (m->ptr64)
-      k_features<long long, B><<<g, B, 0, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                              ptr<unsigned>(bits), ptr<FeatAcc>(acc));
-    else
-      k_features<int, B><<<g, B, 0, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols),
-                                        ptr<unsigned>(bits), ptr<FeatAcc>(acc));
-    SVB_CHECK_LAUNCH();
-    auto* ndiag_d = reinterpret_cast<unsigned long long*>(static_cast<char*>(acc->ptr) + sizeof(FeatAcc));
-    k_popcount<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(bits), ndiag_d);
-    SVB_CHECK_LAUNCH();
-    struct {
-      FeatAcc a;
-      unsigned long long ndiag;
-    } h;
-    SVB_CUDA_TRY(cudaMemcpyAsync(&h, acc->ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
-    SVB_CUDA_TRY(cudaStreamSynchronize(s));
-    {  // complete now: kept for a later DIA conversion of this handle
-      detach(bits);
-      std::lock_guard<std::mutex> lk(m->mu);
-      m->diag_bits = bits;
+    svb_features_job* j = job_get();
+    try {
+      j->m = m;
+      j->s = s;
+      j->cancel_requested = precancelled != 0;
+      cancel_path();   // created before the first job can be cancelled
+      const int64_t nbits = m->nrows + m->ncols - 1;
+      const int64_t nwords = (nbits + 31) / 32;
+      j->bits = alloc(nwords * 4, s);
+      j->out = alloc(sizeof(FeatOut), s);
+      auto* out = ptr<FeatOut>(j->out);
+      SVB_CUDA_TRY(cudaMemsetAsync(j->bits->ptr, 0, nwords * 4, s));
+      SVB_CUDA_TRY(cudaMemsetAsync(out, 0, offsetof(FeatOut, offs), s));
+      const long long big = LLONG_MAX;
+      SVB_CUDA_TRY(cudaMemcpyAsync(&out->a.min_r, &big, 8, cudaMemcpyHostToDevice, s));
+      const int64_t ntiles = (m->nrows + FEAT_R - 1) / FEAT_R;
+      if (precancelled) {   // nothing is read: report the cancellation only
+        const int one = 1;
+        SVB_CUDA_TRY(cudaMemcpyAsync(&out->cancelled, &one, 4, cudaMemcpyHostToDevice, s));
+      } else if (ntiles > 0) {
+        const size_t dsm32 = FEAT_NS * RingLayout<int, FEAT_R, FEAT_CAP, false>::STAGE;
+        const size_t dsm64 = FEAT_NS * RingLayout<long long, FEAT_R, FEAT_CAP, false>::STAGE;
+        static const bool attr = [&] {
+          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm32));
+          SVB_CUDA_TRY(
+              cudaFuncSetAttribute(k_features<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm64));
+          return true;
+        }();
+        (void)attr;
+        const unsigned g = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 3);
+        if (m->ptr64)
+          k_features<long long><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
+                                                          ptr<unsigned>(j->bits), out, j->flag);
+        else
+          k_features<int><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols),
+                                                   ptr<unsigned>(j->bits), out, j->flag);
+        SVB_CHECK_LAUNCH();
+      }
+      k_popcount<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(j->bits), &out->ndiag);
+      SVB_CHECK_LAUNCH();
+      k_bits_to_offsets<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(j->bits), -(m->nrows - 1),
+                                                                out->offs, 4096, &out->noffs, &out->ndiag);
+      SVB_CHECK_LAUNCH();
+      SVB_CUDA_TRY(cudaMemcpyAsync(j->host, out, offsetof(FeatOut, offs), cudaMemcpyDeviceToHost, s));
+      // the offsets only when they fit the DIA cap (a second copy ordered after the first)
+      SVB_CUDA_TRY(cudaMemcpyAsync(j->host->offs, out->offs, sizeof(out->offs), cudaMemcpyDeviceToHost, s));
+      SVB_CUDA_TRY(cudaEventRecord(j->done, s));
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      job_put(j);
+      throw;
     }
-    agg[0] = (int64_t)h.a.sum_r;
-    agg[1] = (int64_t)h.a.sum_r2;
-    agg[2] = h.a.max_r;
-    agg[3] = m->nrows ? h.a.min_r : 0;
-    agg[4] = (int64_t)h.a.span;
-    agg[5] = (int64_t)h.a.runs;
-    agg[6] = (int64_t)h.ndiag;
+    *job = j;
   });
+}
+
+extern "C" int svb_features_cancel(svb_features_job* job) {
+  return guard([&] {
+    SVB_REQUIRE(job, SVB_INVALID, "null job");
+    if (job->cancel_requested) return;
+    job->cancel_requested = true;
+    CancelPath& c = cancel_path();
+    SVB_CUDA_TRY(cudaMemcpyAsync(job->flag, c.one, sizeof(int), cudaMemcpyHostToDevice, c.s));
+  });
+}
+
+extern "C" int svb_features_query(svb_features_job* job, int* done) {
+  return guard([&] {
+    SVB_REQUIRE(job && done, SVB_INVALID, "null job");
+    const cudaError_t e = cudaEventQuery(job->done);
+    if (e == cudaErrorNotReady) {
+      *done = 0;
+      return;
+    }
+    SVB_CUDA_TRY(e);
+    *done = 1;
+  });
+}
+
+extern "C" int svb_features_finish(svb_features_job* job, int64_t* agg, int64_t* counters, int* cancelled) {
+  return guard([&] {
+    SVB_REQUIRE(job, SVB_INVALID, "null job");
+    struct Put {   // the job goes back to the pool whatever happens below
+      svb_features_job* j;
+      ~Put() { job_put(j); }
+    } put{job};
+    SVB_CUDA_TRY(cudaEventSynchronize(job->done));
+    if (job->cancel_requested) {   // re-arm the flag before the job is reused
+      CancelPath& c = cancel_path();
+      SVB_CUDA_TRY(cudaMemsetAsync(job->flag, 0, sizeof(int), c.s));
+      SVB_CUDA_TRY(cudaStreamSynchronize(c.s));
+    }
+    const FeatOut& h = *job->host;
+    const svb_matrix* m = job->m;
+    if (counters) {
+      counters[0] = (int64_t)h.rows_read;
+      counters[1] = (int64_t)h.cols_read;
+    }
+    const int was_cancelled = h.cancelled || job->cancel_requested;
+    if (cancelled) *cancelled = was_cancelled;
+    if (agg) {
+      agg[0] = (int64_t)h.a.sum_r;
+      agg[1] = (int64_t)h.a.sum_r2;
+      agg[2] = h.a.max_r;
+      agg[3] = m->nrows ? h.a.min_r : 0;
+      agg[4] = (int64_t)h.a.span;
+      agg[5] = (int64_t)h.a.runs;
+      agg[6] = (int64_t)h.ndiag;
+    }
+    if (!h.cancelled) {   // complete: kept for a later DIA conversion of this handle
+      detach(job->bits);
+      std::lock_guard<std::mutex> lk(m->mu);
+      m->diag_bits = job->bits;
+      m->diag_offs.clear();
+      m->diag_offs_valid = h.noffs <= 4096;
+      if (m->diag_offs_valid) {
+        m->diag_offs.assign(h.offs, h.offs + h.noffs);
+        std::sort(m->diag_offs.begin(), m->diag_offs.end());
+      }
+    }
+  });
+}
+
+extern "C" int svb_features(const svb_matrix* m, int64_t* agg, void* stream) {
+  svb_features_job* job = nullptr;
+  const int st = svb_features_start(m, 0, stream, &job);
+  if (st != SVB_OK) return st;
+  return svb_features_finish(job, agg, nullptr, nullptr);
 }
 
 extern "C" int svb_diag_offsets(const svb_matrix* m, int64_t shift, int64_t* out_host, int64_t cap, int64_t* count,

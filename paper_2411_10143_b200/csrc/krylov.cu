@@ -1244,6 +1244,25 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
       k->res_smem = (size_t)(k->chunk + 34) * sizeof(double);
       const char* mode = std::getenv("SPMVTUNE_MGS");
       const bool allowed = !(mode && std::strcmp(mode, "stream") == 0);
+      // TMA-streamed MGS: w in registers + smem, V_{i-1} in TMEM, the basis
+      // rows streamed once through a bulk-copy ring.  Its own plan() bounds
+      // it (a slice of at most mgs::MAX_SLICE = 32768 doubles: n <= 4.85 M
+      // on 148 SMs), independent of the older SM-resident kernel's limit
+      const bool tma_ok = !(mode && (std::strcmp(mode, "resident") == 0 || std::strcmp(mode, "tmem") == 0)) &&
+                          m + 2 < 255;
+      if (allowed && coop && m >= 1 && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages) &&
+          mgs::SMEM <= (size_t)optin) {
+        SVB_CUDA_TRY(cudaFuncSetAttribute(mgs::k_mgs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)mgs::SMEM));
+        int per = 0;
+        SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mgs::k_mgs_tma, mgs::NT, mgs::SMEM));
+        if (per >= 1) {
+          k->tma = true;
+          const size_t gb = 2 * (size_t)mgs::SLOT_STRIDE * G * sizeof(unsigned long long);
+          k->gslot = alloc(gb, s);
+          SVB_CUDA_TRY(cudaMemsetAsync(k->gslot->ptr, 0, gb, s));
+        }
+      }
       if (allowed && coop && m >= 1 && k->res_smem <= (size_t)optin) {
         SVB_CUDA_TRY(cudaFuncSetAttribute(k_gm_mgs_resident, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)k->res_smem));
@@ -1257,23 +1276,6 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
         // full 512-column TMEM allocation can never contend
         const bool tmem_ok = !(mode && std::strcmp(mode, "resident") == 0) &&
                              (k->chunk + PB - 1) / PB <= TMEM_MAX_PER_THREAD;
-        // TMA-streamed MGS: w in registers + smem, V_{i-1} in TMEM, the basis
-        // rows streamed once through a bulk-copy ring
-        const bool tma_ok = !(mode && (std::strcmp(mode, "resident") == 0 || std::strcmp(mode, "tmem") == 0)) &&
-                            m + 2 < 255;
-        if (k->resident && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages) &&
-            mgs::SMEM <= (size_t)optin) {
-          SVB_CUDA_TRY(cudaFuncSetAttribute(mgs::k_mgs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)mgs::SMEM));
-          int per = 0;
-          SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mgs::k_mgs_tma, mgs::NT, mgs::SMEM));
-          if (per >= 1) {
-            k->tma = true;
-            const size_t gb = 2 * (size_t)mgs::SLOT_STRIDE * G * sizeof(unsigned long long);
-            k->gslot = alloc(gb, s);
-            SVB_CUDA_TRY(cudaMemsetAsync(k->gslot->ptr, 0, gb, s));
-          }
-        }
         if (k->resident && tmem_ok) {
           k->tmem_smem = std::max<size_t>(k->res_smem, 120 * 1024);
           if (k->tmem_smem <= (size_t)optin) {

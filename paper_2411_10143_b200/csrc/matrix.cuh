@@ -49,6 +49,10 @@ struct svb_matrix {
   // CSR: the diagonal-occupancy bitmap svb_features built (bit c - i + n - 1),
   // reused by the DIA conversion instead of a second pass over col_idx
   mutable svb::Buf diag_bits;
+  // ... and the sorted diagonal offsets of that bitmap when there are at
+  // most DIA_OFFSET_CAP of them (the DIA conversion skips its offset scan)
+  mutable bool diag_offs_valid = false;
+  mutable std::vector<int64_t> diag_offs;
 
   int64_t device_bytes() const {
     int64_t b = 0;
@@ -133,21 +137,91 @@ __device__ __forceinline__ StagedRows<P> stage_row_tile(int64_t tile, int64_t nr
   return t;
 }
 
+// ---------------------------------------------------------------------------
+// Row-tile ring: fixed R-row tiles (tile t = rows [tR, min((t+1)R, n))) whose
+// row-pointer slice and, when the tile's entries fit CAP, col_idx range
+// (and optionally the values) are bulk-copied (TMA engine, mbarrier
+// completion) into an NS-stage shared-memory ring by one thread, so NS-1
+// tiles are in flight while one is walked.  The synchronous stage_row_tile
+// keeps one 4-byte load per thread in flight; the ring keeps ~NS x 10-40 KB
+// per CTA in flight, which is what HBM needs (Little's law: ~45 KB per SM).
+// Copies are 16-B aligned supersets (device buffers carry a 128-B tail).
+// ---------------------------------------------------------------------------
+template <class P, int R, int CAP, bool VALS>
+struct RingLayout {
+  static constexpr size_t SV = VALS ? (size_t)(CAP + 8) * 8 : 0;
+  static constexpr size_t SC = (size_t)(CAP + 8) * 4;
+  static constexpr size_t SP = ((size_t)(R + 1) * sizeof(P) + 32 + 15) / 16 * 16;
+  static constexpr size_t STAGE = (SV + SC + SP + 127) / 128 * 128;
+};
+
+struct RingDesc {
+  int64_t r0, r1, e0, e1;  // rows [r0, r1), entries [e0, e1)
+  int poff, coff, voff;    // element offsets of r0 / e0 inside the staged supersets
+  int staged;              // cols (and vals) staged; otherwise read from global
+};
+
+__device__ __forceinline__ uintptr_t align_dn16(const void* p) { return (uintptr_t)p & ~(uintptr_t)15; }
+__device__ __forceinline__ uintptr_t align_up16(const void* p) {
+  return ((uintptr_t)p + 15) & ~(uintptr_t)15;
+}
+
+// One thread: arm `bar` and bulk-copy tile [r0, r1) (entries [e0, e1)) into `stage`.
+template <class P, int R, int CAP, bool VALS>
+__device__ __forceinline__ void ring_issue(unsigned char* stage, uint64_t* bar, RingDesc* d, int64_t r0, int64_t r1,
+                                           int64_t e0, int64_t e1, const P* ptr, const int* cols,
+                                           const double* vals, uint64_t policy) {
+  using Lay = RingLayout<P, R, CAP, VALS>;
+  const uintptr_t pa = align_dn16(ptr + r0);
+  const uint32_t np = (uint32_t)(align_up16(ptr + r1 + 1) - pa);
+  uint32_t nc = 0, nv = 0;
+  uintptr_t ca = 0, va = 0;
+  int coff = 0, voff = 0;
+  if (e1 > e0) {
+    ca = align_dn16(cols + e0);
+    nc = (uint32_t)(align_up16(cols + e1) - ca);
+    coff = (int)(((uintptr_t)(cols + e0) - ca) / 4);
+    if (VALS) {
+      va = align_dn16(vals + e0);
+      nv = (uint32_t)(align_up16(vals + e1) - va);
+      voff = (int)(((uintptr_t)(vals + e0) - va) / 8);
+    }
+  }
+  const bool staged = nc <= Lay::SC && nv <= Lay::SV;
+  if (!staged) nc = nv = 0;
+  *d = RingDesc{r0, r1, e0, e1, (int)(((uintptr_t)(ptr + r0) - pa) / sizeof(P)), coff, voff, staged ? 1 : 0};
+  mbar_expect_tx(bar, np + nc + nv);
+  bulk_g2s(stage + Lay::SV + Lay::SC, reinterpret_cast<const void*>(pa), np, bar);
+  if (nc) bulk_g2s_hint(stage + Lay::SV, reinterpret_cast<const void*>(ca), nc, bar, policy);
+  if (nv) bulk_g2s_hint(stage, reinterpret_cast<const void*>(va), nv, bar, policy);
+}
+
 // Diagonal-occupancy bitmap marking with a per-CTA direct-mapped cache of
 // diagonal indices already set: a stencil or banded matrix touches a handful
 // of diagonals, so nearly every entry hits the cache and the global bitmap
-// sees one read/atomicOr per (CTA, diagonal) instead of one per entry.
+// sees one atomicOr per (CTA, diagonal) instead of one per entry.
 constexpr int DIAG_CACHE = 512;
 __device__ __forceinline__ void diag_cache_init(long long* cache) {
   for (int k = threadIdx.x; k < DIAG_CACHE; k += blockDim.x) cache[k] = -1;
 }
 __device__ __forceinline__ void mark_diag(unsigned* __restrict__ bits, long long d, long long* cache) {
   const int slot = (int)(d & (DIAG_CACHE - 1));
-  if (*(volatile long long*)(cache + slot) == d) return;
+  const long long old = *(volatile long long*)(cache + slot);
+  if (old == d) return;
   const unsigned m = 1u << (d & 31);
   unsigned* w = bits + (d >> 5);
-  if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
-  cache[slot] = d;   // racy but benign: a stale slot only costs a global check
+  if (old < 0) {
+    // first use of the slot (a stencil's few hot diagonals, every CTA at
+    // once): test before setting, so the diagonal's word sees reads, not
+    // thousands of same-address atomics
+    if (!(*(volatile unsigned*)w & m)) atomicOr(w, m);
+  } else {
+    // an eviction: diagonals spread over millions of words (power-law) —
+    // fire-and-forget (RED, result unused), no L2 round trip on the
+    // thread's critical path
+    atomicOr(w, m);
+  }
+  cache[slot] = d;   // racy but benign: a stale slot only costs a global update
 }
 
 }  // namespace svb

@@ -7,15 +7,18 @@ here with the reference's own expressions and operation order
 (features.py:103-110, 147-150), which makes the vector bit-identical to the
 CPU path.
 
-Cancellation keeps the reference contract: a flag raised before the call
-returns ``None`` without touching ``col_idx``; a flag raised while the
-extraction runs is honoured at the phase boundaries (after the device pass
-and before the float evaluation).
+Cancellation keeps the reference contract (features.py:60-65, 89-91): a
+flag raised before the call returns ``None`` without reading ``row_ptr`` or
+``col_idx``; a flag raised while the pass runs is forwarded to the device
+(a host-mapped word the kernel polls once per 256-row tile), which then
+stops reading, and the call returns ``None``.  The traversal counters report
+the row_ptr and col_idx elements the device pass actually read.
 """
 from __future__ import annotations
 
 import ctypes
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -101,21 +104,39 @@ def extract_features(m: CsrMatrix, cancel: threading.Event | None = None, *,
                      row_chunk: int = CANCEL_CHECK_ROWS, stream=None) -> FeatureVector | None:
     """Feature vector of ``m`` or ``None`` when ``cancel`` is (or becomes) set.
 
-    ``row_chunk`` is accepted for API parity; the device pass is not chunked
-    (it streams row_ptr and col_idx exactly once, so the counters report one
-    pass over each array plus the reference's second row_ptr scan)."""
+    The device pass runs as a job (svb_features_start); while it runs this
+    thread polls ``cancel`` and forwards a raised flag to the kernel, which
+    stops at its next 256-row tile — the device analogue of the reference's
+    check every ``row_chunk`` rows (accepted for API parity)."""
     if cancel is not None and cancel.is_set():
         return None
     if not isinstance(m, CsrMatrix):
         raise TypeError("extract_features expects a CsrMatrix")
-    agg = device_aggregates(m, stream)
+    L = _lib.lib()
+    job = ctypes.c_void_p()
+    _lib.check(L.svb_features_start(m._device().handle, 0, stream.handle if stream is not None else None,
+                                    ctypes.byref(job)))
+    agg = (ctypes.c_int64 * 7)()
+    cnt = (ctypes.c_int64 * 2)()
+    was = ctypes.c_int32(0)
+    try:
+        if cancel is not None:
+            done = ctypes.c_int32(0)
+            forwarded = False
+            while True:
+                _lib.check(L.svb_features_query(job, ctypes.byref(done)))
+                if done.value:
+                    break
+                if forwarded:
+                    time.sleep(20e-6)
+                elif cancel.wait(50e-6):
+                    _lib.check(L.svb_features_cancel(job))
+                    forwarded = True
+    finally:
+        _lib.check(L.svb_features_finish(job, agg, cnt, ctypes.byref(was)))
     if counter is not None:
-        counter.row_ptr_reads += m.nrows + 1
-    if cancel is not None and cancel.is_set():
+        counter.row_ptr_reads += int(cnt[0])
+        counter.col_idx_reads += int(cnt[1])
+    if was.value or (cancel is not None and cancel.is_set()):
         return None
-    if counter is not None:
-        counter.col_idx_reads += m.nnz
-        counter.row_ptr_reads += m.nrows + 1
-    if cancel is not None and cancel.is_set():
-        return None
-    return features_from_aggregates(m.nrows, m.ncols, m.nnz, agg)
+    return features_from_aggregates(m.nrows, m.ncols, m.nnz, tuple(int(v) for v in agg))

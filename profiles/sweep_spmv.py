@@ -3,7 +3,7 @@
 launching stream, achieved GB/s from the algorithmic bytes of SURVEY.md §8(d)
 against the measured HBM copy peak.
 
-    python profiles/sweep_spmv.py [runs] > profiles/r1_spmv_sweep.json
+    python profiles/sweep_spmv.py [runs] [poisson1024,convdiff2000,powerlaw2M,powerlaw8M] > out.json
 """
 import json
 import os
@@ -54,8 +54,12 @@ def stencil(kind):
 
 
 def main():
-    mats = {"config1_poisson1024": stencil("poisson1024"), "config2_convdiff2000": stencil("cd"),
-            "powerlaw_2M": P.CsrMatrix(*G.powerlaw_spd(2_000_000, seed=0))}
+    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["poisson1024", "convdiff2000", "powerlaw2M"]
+    build = {"poisson1024": ("config1_poisson1024", lambda: stencil("poisson1024")),
+             "convdiff2000": ("config2_convdiff2000", lambda: stencil("cd")),
+             "powerlaw2M": ("powerlaw_2M", lambda: P.CsrMatrix(*G.powerlaw_spd(2_000_000, seed=0))),
+             "powerlaw8M": ("config3_powerlaw_8M", lambda: G.powerlaw_spd_device(8_000_000, seed=0))}
+    mats = {build[w][0]: build[w][1]() for w in which}
     s = device.thread_stream()
     ext = torch.cuda.ExternalStream(s.handle)
     out = {"peak_gbs": PEAK, "runs": RUNS, "results": {}}

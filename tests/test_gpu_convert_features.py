@@ -114,6 +114,36 @@ def test_feature_cancellation_and_counters():
     assert P.extract_features(csr, cancel, counter=Tripping(), row_chunk=16) is None
 
 
+def test_device_cancel_flag_stops_the_pass():
+    """The cancel flag is device-visible: raised after the job is enqueued but
+    before its kernel runs (the stream is held by a spin kernel), the pass
+    reads no row_ptr/col_idx element and reports the cancellation; the next
+    uncancelled pass on the same handle is complete and exact."""
+    import ctypes
+    torch = pytest.importorskip("torch")
+    from paper_2411_10143_b200 import _lib, device
+    n, m, ptr, cols, vals = G.convdiff9(300)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    L = _lib.lib()
+    s = device.thread_stream()
+    h = csr._device().handle
+    with torch.cuda.stream(torch.cuda.ExternalStream(s.handle)):
+        torch.cuda._sleep(20_000_000)        # hold the stream ~10 ms
+    job = ctypes.c_void_p()
+    _lib.check(L.svb_features_start(h, 0, s.handle, ctypes.byref(job)))
+    _lib.check(L.svb_features_cancel(job))
+    agg, cnt, was = (ctypes.c_int64 * 7)(), (ctypes.c_int64 * 2)(), ctypes.c_int32(0)
+    _lib.check(L.svb_features_finish(job, agg, cnt, ctypes.byref(was)))
+    assert was.value == 1 and cnt[0] == 0 and cnt[1] == 0
+    ctr = TraversalCounter()
+    fv = P.extract_features(csr, threading.Event(), counter=ctr)
+    assert fv.to_array().tolist() == O.features(O.OCsr(n, m, ptr, cols, vals))
+    assert ctr.col_idx_reads == csr.nnz
+    dia = P.convert(csr, P.FormatTag.DIA)      # from the offsets the pass left on the handle
+    want = O.convert(O.OCsr(n, m, ptr, cols, vals), "DIA")
+    assert np.array_equal(dia.offsets, want.offsets) and np.array_equal(dia.data, want.data)
+
+
 def test_device_stencil_generator_matches_host():
     for dims, gen in (((30, 30), G.poisson2d(30)), ((25, 25), G.convdiff9(25)),
                       ((9, 9, 9), G.laplace27(9))):

@@ -159,6 +159,47 @@ def test_config2_every_arnoldi_fallback(mode):
     assert r["converged"] and abs(r["iterations"] - g["iterations"]) <= 1 and r["final"] <= 1e-8
 
 
+_MGS_GATE_SCRIPT = r"""
+import json, sys, itertools
+sys.path.insert(0, {root!r})
+import paper_2411_10143_b200 as P
+from paper_2411_10143_b200 import _lib
+offs, w = [], []
+for o in itertools.product((-1, 0, 1), repeat=2):
+    offs.append(o); w.append(8.5 if not any(o) else -1.0 - 0.25 * (o[1] + o[0]))
+A = P.CsrMatrix.stencil(({nx}, {nx}), offs, w)
+params = P.GmresParams(restart_m=30, tol=1e-8, max_iters=1000)
+cfg = P.SpmvConfig(P.FormatTag.DIA, P.Library.LIB_A)
+P.gmres_solve(A, None, P.GmresParams(restart_m=30, tol=1e-8, max_iters=3), initial_config=cfg)
+l0 = _lib.launch_count()
+r = P.gmres_solve(A, None, params, initial_config=cfg)
+print(json.dumps({{"iterations": r.iterations, "converged": r.converged, "final": r.final_residual,
+                  "launches": _lib.launch_count() - l0}}))
+"""
+
+
+def test_tma_arnoldi_beyond_the_resident_kernels_limit():
+    """n = 2180^2 = 4.75 M rows: above the SM-resident kernel's shared-memory
+    bound (~4.29 M) but within the TMA kernel's own (148 x 32768 = 4.85 M):
+    the TMA/TMEM Arnoldi kernel runs (a few launches per step, not one per MGS
+    pass) and lands within 1 iteration of the streaming fallback."""
+    res = {}
+    for mode in ("default", "stream"):
+        env = dict(os.environ)
+        env.pop("SPMVTUNE_MGS", None)
+        if mode == "stream":
+            env["SPMVTUNE_MGS"] = "stream"
+        out = subprocess.run([sys.executable, "-c", _MGS_GATE_SCRIPT.format(root=str(ROOT), nx=2180)], env=env,
+                             capture_output=True, text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
+    a, b = res["default"], res["stream"]
+    assert a["converged"] and b["converged"] and a["final"] <= 1e-8 and b["final"] <= 1e-8
+    assert abs(a["iterations"] - b["iterations"]) <= 1
+    # streaming: one launch per MGS pass (j + 2 per step); TMA: one per step
+    assert a["launches"] / a["iterations"] < 6 < b["launches"] / b["iterations"], res
+
+
 def test_config1_cg_matches_oracle_iterations():
     c = fixtures()["config1"]["cg"]
     A = matrix("config1")
