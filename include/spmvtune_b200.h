@@ -227,10 +227,12 @@ int svb_spmv_sequential(const svb_matrix* csr, const double* x_dev, double* y_de
 int svb_features(const svb_matrix* csr, int64_t* agg_host, void* stream);
 /* The same pass as a job, for extract_features(csr, cancel, counter=...)
  * (features.py:68-156): start enqueues it on `stream` and returns at once;
- * cancel raises a host-mapped flag the kernel polls once per 256-row tile
+ * cancel raises a device flag the kernel polls once per 256-row tile
  * (it then stops reading row_ptr/col_idx; the reference checks every
- * row_chunk rows, features.py:89-91); query reports completion without
- * blocking; finish waits, writes agg[7], counters[2] = {row_ptr elements,
+ * row_chunk rows, features.py:89-91) and may be called from any thread
+ * while another blocks in wait; query reports completion without
+ * blocking; wait blocks until the pass ends (no result, the job stays
+ * live); finish waits, writes agg[7], counters[2] = {row_ptr elements,
  * col_idx elements} actually read (TraversalCounter, features.py:60-65) and
  * *cancelled, and releases the job.  precancelled != 0 reads nothing.  An
  * uncancelled pass leaves its diagonal bitmap and sorted offsets on the
@@ -239,6 +241,7 @@ typedef struct svb_features_job svb_features_job;
 int svb_features_start(const svb_matrix* csr, int precancelled, void* stream, svb_features_job** job);
 int svb_features_cancel(svb_features_job* job);
 int svb_features_query(svb_features_job* job, int* done);
+int svb_features_wait(svb_features_job* job);
 int svb_features_finish(svb_features_job* job, int64_t* agg_host, int64_t* counters_host, int* cancelled);
 /* The distinct diagonal offsets (col - row) of a CSR handle plus `shift`,
  * ascending (the ndiag feature's set, features.py:118-126; a row-partitioned
@@ -328,13 +331,16 @@ int svb_vec_axpby(svb_vecops* v, double a, const double* x_dev, double b, double
 /* x *= s */
 int svb_vec_scale(svb_vecops* v, double* x_dev, double s, void* stream);
 /* Row-partitioned CG on device scalars sc[] (NCCL all-reduces them in place
- * between calls): x += a p, r -= a q, a = sc[irr]/sc[ipq], local r.r ->
- * sc[out] (a zero/non-finite sc[ipq] leaves x, r untouched); then
- * p = r + (sc[inew]/sc[iold]) p.  Oracle: oracle/cpu_oracle.py:cg. */
-int svb_dcg_update(svb_vecops* v, double* sc_dev, int32_t irr, int32_t ipq, int32_t out, const double* p_dev,
-                   const double* q_dev, double* x_dev, double* r_dev, void* stream);
-int svb_dcg_p(svb_vecops* v, const double* sc_dev, int32_t inew, int32_t iold, const double* r_dev,
-              double* p_dev, void* stream);
+ * between calls), the two vector passes that follow the SpMV + p.Ap pass:
+ *   svb_dcg_rupdate: a = sc[icur]/sc[ipq] -> sc[ialpha], r -= a q, local
+ *                    r.r -> sc[out] (a zero/non-finite sc[ipq]: a = 0, r
+ *                    untouched, sc[out] = sc[icur]);
+ *   svb_dcg_xp:      x += sc[ialpha] p, then p = r + (sc[inew]/sc[iold]) p.
+ * Oracle: oracle/cpu_oracle.py:cg (x += a p; r -= a q; p = r + b p). */
+int svb_dcg_rupdate(svb_vecops* v, double* sc_dev, int32_t icur, int32_t ipq, int32_t out, int32_t ialpha,
+                    const double* q_dev, double* r_dev, void* stream);
+int svb_dcg_xp(svb_vecops* v, const double* sc_dev, int32_t ialpha, int32_t inew, int32_t iold,
+               const double* r_dev, double* p_dev, double* x_dev, void* stream);
 /* y = A x in the configuration, fused with *out_dev = dsrc . y (CG's p.Ap,
  * oracle/cpu_oracle.py:cg) — one pass for DIA (the dot folded into the
  * TMA-staged SpMV), SpMV + dot otherwise; `accumulate` adds into *out_dev

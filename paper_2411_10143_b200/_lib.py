@@ -100,8 +100,8 @@ _SIGS = {
     "svb_mm_close": [_P],
     "svb_coo_from_triplets": [C.c_int64, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, _PP],
     "svb_event_sync": [_P],
-    "svb_dcg_update": [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],
-    "svb_dcg_p": [_P, _P, C.c_int32, C.c_int32, _P, _P, _P],
+    "svb_dcg_rupdate": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "svb_dcg_xp": [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "svb_cg_step_batched_dia": [_P, _P, C.c_double, _P],
     "svb_krylov_mark": [_P, _P],
     "svb_graph_begin": [_P],
@@ -131,6 +131,7 @@ _SIGS = {
     "svb_features_start": [_P, C.c_int, _P, _PP],
     "svb_features_cancel": [_P],
     "svb_features_query": [_P, C.POINTER(C.c_int32)],
+    "svb_features_wait": [_P],
     "svb_features_finish": [_P, _PI64, _PI64, C.POINTER(C.c_int32)],
     "svb_krylov_create": [_I64, _I32, _PP],
     "svb_krylov_destroy": [_P],

@@ -65,9 +65,9 @@ constexpr int FEAT_LONG = 64;
 // Longest run of consecutive columns and the diagonal marks of one row by a
 // warp, in the sequential recurrence's terms (run = c == prev + 1 ? run + 1
 // : 1, best = max run); returns (best, last - first column) on every lane.
-template <class G>
-__device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e, int64_t diag0,
-                                              unsigned* __restrict__ bits, long long* dcache,
+template <class D, class G>
+__device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e, D diag0,
+                                              unsigned* __restrict__ bits, D* dcache,
                                               long long* best_out, long long* span_out) {
   const int lane = threadIdx.x & 31;
   long long best = 0, carry = 0;   // run length through the previous chunk's last entry
@@ -81,7 +81,7 @@ __device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e
     int pc = __shfl_up_sync(0xffffffffu, c, 1);
     if (lane == 0) pc = prev_last;
     const bool brk = valid && ((k == s) || c != pc + 1);
-    if (valid) mark_diag(bits, (long long)c + diag0, dcache);
+    if (valid) mark_diag(bits, (D)c + diag0, dcache);
     const unsigned B = __ballot_sync(0xffffffffu, brk);
     const unsigned upto = B & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
     long long run = 0;
@@ -101,15 +101,21 @@ __device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e
 
 // One pass over row_ptr and col_idx through the row-tile ring (matrix.cuh):
 // one thread per row walks its staged columns (run lengths, span, diagonal
-// marks); rows longer than FEAT_LONG go to a warp.  Thread 0 polls the
-// cancel flag one tile ahead and, once it is raised, stops refilling the
-// ring; the tiles already in flight are drained without being walked.  The
-// flag is a device word (an L2 read per tile): svb_features_cancel raises it
-// with a 4-byte copy on a side stream, which the copy engine performs while
-// the kernel runs.  (Polling host-mapped memory instead costs a PCIe round
-// trip per tile, and those reads serialise: 12 ms for a 4 M-row pass.)  Rows and entries actually
-// walked are counted (the reference's TraversalCounter, features.py:60-65).
-constexpr int FEAT_R = 256, FEAT_CAP = 3072, FEAT_NS = 3;
+// marks) in 32-bit arithmetic (ncu, round 1 kernel: 65 instructions per
+// entry, issue-bound at 0.2 of HBM); rows longer than FEAT_LONG go to a
+// warp.  A tile's entries are staged up to the stage capacity (a row that
+// crosses the end reads global memory).  Thread 0 keeps the row-pointer
+// bounds of the tiles it will issue FEAT_PF tiles ahead with cp.async, so
+// no refill waits on a dependent row_ptr load.  Thread 0 polls the cancel
+// flag one tile ahead and, once it is raised, stops refilling the ring; the
+// tiles already in flight are drained without being walked.  The flag is a
+// device word (an L2 read per tile): svb_features_cancel raises it with a
+// 4-byte copy on a side stream, which the copy engine performs while the
+// kernel runs.  (Polling host-mapped memory instead costs a PCIe round trip
+// per tile, and those reads serialise: 12 ms for a 4 M-row pass.)  Rows and
+// entries actually walked are counted (the reference's TraversalCounter,
+// features.py:60-65).
+constexpr int FEAT_R = 256, FEAT_CAP = 5120, FEAT_NS = 3, FEAT_PF = 4, FEAT_BR = 8;
 
 struct FeatOut {
   FeatAcc a;
@@ -121,7 +127,7 @@ struct FeatOut {
   long long offs[4096];                      // diagonal offsets (unordered) when ndiag <= 4096
 };
 
-template <class P>
+template <class P, class D>
 __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __restrict__ ptr,
                                                      const int* __restrict__ cols, unsigned* __restrict__ bits,
                                                      FeatOut* out, const volatile int* cancel) {
@@ -129,8 +135,9 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ alignas(8) uint64_t bar[FEAT_NS];
   __shared__ RingDesc desc[FEAT_NS];
-  __shared__ long long dcache[DIAG_CACHE];
+  __shared__ D dcache[DIAG_CACHE];
   __shared__ int lrows[FEAT_R];
+  __shared__ alignas(16) P bnd[FEAT_BR][2];   // entry bounds of prefetched tiles
   __shared__ int nlong[2], sstop;   // long-row count, double-buffered by iteration parity
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   diag_cache_init(dcache);
@@ -142,9 +149,14 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
     ring_issue<P, FEAT_R, FEAT_CAP, false>(ring + st * Lay::STAGE, &bar[st], &desc[st], r0, r1, e0, e1, ptr, cols,
                                           nullptr, policy);
   };
-  auto bounds_of = [&](int64_t tile, int64_t& e0, int64_t& e1) {
-    e0 = (int64_t)ptr[tile * FEAT_R];
-    e1 = (int64_t)ptr[min(tile * FEAT_R + FEAT_R, nrows)];
+  auto prefetch = [&](int64_t local) {   // bounds of this CTA's local-th tile -> bnd (thread 0)
+    const int64_t tile = blockIdx.x + local * gridDim.x;
+    if (tile < ntiles) {
+      const int sl = (int)(local % FEAT_BR);
+      cp_async_small<sizeof(P)>(&bnd[sl][0], ptr + tile * FEAT_R);
+      cp_async_small<sizeof(P)>(&bnd[sl][1], ptr + min(tile * FEAT_R + FEAT_R, nrows));
+    }
+    cp_async_commit();   // one group per call, empty or not: wait_group counts them
   };
   if (tid == 0) {
     nlong[0] = nlong[1] = 0;
@@ -153,13 +165,11 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
     if (cancel) cflag = *cancel;
     for (int st = 0; st < FEAT_NS; ++st) {
       const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
-      if (tile < ntiles && !cflag) {
-        int64_t e0, e1;
-        bounds_of(tile, e0, e1);
-        issue(st, tile, e0, e1);
-      }
+      if (tile < ntiles && !cflag)
+        issue(st, tile, (int64_t)ptr[tile * FEAT_R], (int64_t)ptr[min(tile * FEAT_R + FEAT_R, nrows)]);
     }
     if (cflag) sstop = 1;
+    for (int k = 0; k < FEAT_PF; ++k) prefetch(FEAT_NS + k);
   }
   __syncthreads();
   FeatAcc a{0, 0, 0, 0, 0, LLONG_MAX};
@@ -170,11 +180,10 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
     int& nl = nlong[it & 1];
     int nxt_cancel = 0;
     const int64_t tn = tile + (int64_t)FEAT_NS * gridDim.x;   // the tile this stage takes next
-    int64_t ne0 = 0, ne1 = 0;
     if (tid == 0) {
       nlong[(it + 1) & 1] = 0;   // last read before the previous iteration's final barrier
       if (cancel) nxt_cancel = *cancel;   // consumed after this tile (latency hidden)
-      if (tn < ntiles) bounds_of(tn, ne0, ne1);   // likewise: used by the refill below
+      prefetch(it + FEAT_NS + FEAT_PF);
     }
     mbar_wait(&bar[st], (uint32_t)(it / FEAT_NS) & 1u);
     const RingDesc d = desc[st];
@@ -182,7 +191,8 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
     const unsigned char* stage = ring + st * Lay::STAGE;
     const int* scol = reinterpret_cast<const int*>(stage + Lay::SV) + d.coff;
     const P* sp = reinterpret_cast<const P*>(stage + Lay::SV + Lay::SC) + d.poff;
-    auto col = [&](int64_t k) { return d.staged ? scol[k] : __ldg(cols + d.e0 + k); };
+    const int64_t nst = d.staged;
+    auto col = [&](int64_t k) { return k < nst ? scol[k] : __ldg(cols + d.e0 + k); };
     const int64_t i = d.r0 + tid;
     if (walk && i < d.r1) {
       const int64_t s = (int64_t)sp[tid] - d.e0, e = (int64_t)sp[tid + 1] - d.e0, L = e - s;
@@ -193,19 +203,22 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
       if (L > FEAT_LONG) {
         lrows[atomicAdd(&nl, 1)] = tid;
       } else if (L > 0) {
-        const int64_t diag0 = nrows - 1 - i;
-        const int c0 = col(s);
-        int prev = c0;
-        int64_t run = 1, best = 1;
-        for (int64_t k = s;;) {
-          mark_diag(bits, (long long)prev + diag0, dcache);
-          if (++k >= e) break;
-          const int c = col(k);
+        // 32-bit walk over the row's columns (shared memory when the whole
+        // row is staged)
+        const int* rp = e <= nst ? scol + s : cols + d.e0 + s;
+        const int n = (int)L;
+        const D dg = (D)(nrows - 1 - i);
+        const int c0 = rp[0];
+        int prev = c0, run = 1, best = 1;
+        mark_diag(bits, (D)c0 + dg, dcache);
+        for (int k = 1; k < n; ++k) {
+          const int c = rp[k];
           run = (c == prev + 1) ? run + 1 : 1;
           best = max(best, run);
+          mark_diag(bits, (D)c + dg, dcache);
           prev = c;
         }
-        a.span += (unsigned long long)(prev - c0);
+        a.span += (unsigned long long)((long long)prev - c0);
         a.runs += (unsigned long long)best;
       }
     }
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
       const int64_t r = d.r0 + lrows[q];
       const int64_t s = (int64_t)sp[lrows[q]] - d.e0, e = (int64_t)sp[lrows[q] + 1] - d.e0;
       long long best, span;
-      warp_row_runs(col, s, e, nrows - 1 - r, bits, dcache, &best, &span);
+      warp_row_runs(col, s, e, (D)(nrows - 1 - r), bits, dcache, &best, &span);
       if (lane == 0) {
         a.span += (unsigned long long)span;
         a.runs += (unsigned long long)best;
@@ -232,11 +245,15 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
     if (sstop && stop_at == INT64_MAX) stop_at = it + FEAT_NS;   // drain what is in flight
     if (tid == 0) {
       if (!sstop && tn < ntiles) {
+        cp_async_wait<FEAT_PF>();   // this tile's bounds (prefetched FEAT_PF tiles ago) landed
+        const int sl = (int)((it + FEAT_NS) % FEAT_BR);
+        const int64_t e0 = (int64_t)bnd[sl][0], e1 = (int64_t)bnd[sl][1];
         fence_proxy_async_smem();
-        issue(st, tn, ne0, ne1);
+        issue(st, tn, e0, e1);
       }
     }
   }
+  cp_async_wait<0>();
   block_reduce_store<FEAT_R>(a, &out->a);
   if (tid == 0) {
     if (rows_read) atomicAdd(&out->rows_read, rows_read);
@@ -393,19 +410,36 @@ extern "C" int svb_features_start(const svb_matrix* m, int precancelled, void* s
         const size_t dsm32 = FEAT_NS * RingLayout<int, FEAT_R, FEAT_CAP, false>::STAGE;
         const size_t dsm64 = FEAT_NS * RingLayout<long long, FEAT_R, FEAT_CAP, false>::STAGE;
         static const bool attr = [&] {
-          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm32));
-          SVB_CUDA_TRY(
-              cudaFuncSetAttribute(k_features<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm64));
+          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<int, unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)dsm32));
+          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<int, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)dsm32));
+          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<long long, unsigned>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm64));
+          SVB_CUDA_TRY(cudaFuncSetAttribute(k_features<long long, long long>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm64));
           return true;
         }();
         (void)attr;
         const unsigned g = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 3);
-        if (m->ptr64)
-          k_features<long long><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                                          ptr<unsigned>(j->bits), out, j->flag);
-        else
-          k_features<int><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols),
-                                                   ptr<unsigned>(j->bits), out, j->flag);
+        // 32-bit diagonal indices whenever they fit (nrows + ncols - 1 < 2^32)
+        const bool narrow = nbits < (int64_t(1) << 32);
+        auto* bitsp = ptr<unsigned>(j->bits);
+        if (m->ptr64) {
+          if (narrow)
+            k_features<long long, unsigned><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
+                                                                     bitsp, out, j->flag);
+          else
+            k_features<long long, long long><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr),
+                                                                      ptr<int>(m->cols), bitsp, out, j->flag);
+        } else {
+          if (narrow)
+            k_features<int, unsigned><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols), bitsp,
+                                                               out, j->flag);
+          else
+            k_features<int, long long><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols), bitsp,
+                                                                out, j->flag);
+        }
         SVB_CHECK_LAUNCH();
       }
       k_popcount<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(j->bits), &out->ndiag);
@@ -446,6 +480,13 @@ extern "C" int svb_features_query(svb_features_job* job, int* done) {
     }
     SVB_CUDA_TRY(e);
     *done = 1;
+  });
+}
+
+extern "C" int svb_features_wait(svb_features_job* job) {
+  return guard([&] {
+    SVB_REQUIRE(job, SVB_INVALID, "null job");
+    SVB_CUDA_TRY(cudaEventSynchronize(job->done));
   });
 }
 

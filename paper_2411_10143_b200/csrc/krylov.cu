@@ -1007,25 +1007,27 @@ __global__ void __launch_bounds__(KB) k_dot_acc(int64_t n, const double* __restr
   if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) *out = accumulate ? *out + tot : tot;
 }
 
-// Row-partitioned CG, fused on device scalars sc[] (all-reduced in place
-// between the kernels): x += a p, r -= a q with a = sc[irr]/sc[ipq], and the
-// local r.r into sc[out].  A zero or non-finite p.Ap leaves x and r untouched
-// (the host then confirms with the true residual or reports the breakdown,
-// as in the unfused loop) and copies r.r through unchanged.
-__global__ void __launch_bounds__(KB) k_dcg_update(int64_t n, double* sc, int irr, int ipq, int out,
-                                                   const double* __restrict__ p, const double* __restrict__ q,
-                                                   double* __restrict__ x, double* __restrict__ r, double* partials,
-                                                   unsigned* counter) {
+// Row-partitioned CG on device scalars sc[] (all-reduced in place between
+// the kernels), two vector passes per iteration after the SpMV+p.q pass:
+//   k_dcg_rupdate: a = sc[icur]/sc[ipq] -> sc[ialpha], r -= a q, local r.r
+//                  -> sc[out]  (reads r, q; writes r: 24 B/row)
+//   k_dcg_xp:      x += a p, then p = r + b p with b = sc[inew]/sc[iold]
+//                  (reads x, r, p; writes x, p: 40 B/row)
+// i.e. the unfused x/r update + p update (48 + 24 B/row) regrouped so x
+// moves in the pass that rewrites p, which reads p anyway.  A zero or
+// non-finite p.Ap stores a = 0 and leaves r untouched (x then stays put too;
+// the host confirms with the true residual or reports the breakdown) and
+// copies r.r through unchanged.  Expressions are the contracted forms of
+// the oracle loop's (oracle/cpu_oracle.py:cg): x + a p, r - a q, r + b p.
+__global__ void __launch_bounds__(KB) k_dcg_rupdate(int64_t n, double* sc, int icur, int ipq, int out, int ialpha,
+                                                    const double* __restrict__ q, double* __restrict__ r,
+                                                    double* partials, unsigned* counter) {
   const double pq = sc[ipq];
   const bool ok = pq != 0.0 && isfinite(pq);
-  const double a = ok ? sc[irr] / pq : 0.0;
+  const double a = ok ? sc[icur] / pq : 0.0;
   double acc = 0.0;
-  // p may be a slice of a halo window at an odd element offset: pairs only
-  // when every operand is 16-byte aligned
-  const bool al = (((uintptr_t)p | (uintptr_t)q | (uintptr_t)x | (uintptr_t)r) & 15) == 0;
-  if (ok && !al) {
+  if (ok && (((uintptr_t)q | (uintptr_t)r) & 15) != 0) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-      x[e] = x[e] + a * p[e];
       const double rn = r[e] - a * q[e];
       r[e] = rn;
       acc += rn * rn;
@@ -1034,39 +1036,51 @@ __global__ void __launch_bounds__(KB) k_dcg_update(int64_t n, double* sc, int ir
     for_pairs(
         n,
         [&](int64_t e) {
-          const double2 pp = ld2(p + e), qq = ld2(q + e), xx = ld2(x + e), rr = ld2(r + e);
+          const double2 qq = ld2(q + e), rr = ld2(r + e);
           const double2 rn = make_double2(rr.x - a * qq.x, rr.y - a * qq.y);
-          st2(x + e, make_double2(xx.x + a * pp.x, xx.y + a * pp.y));
           st2(r + e, rn);
           acc += rn.x * rn.x + rn.y * rn.y;
         },
         [&](int64_t e) {
-          x[e] = x[e] + a * p[e];
           const double rn = r[e] - a * q[e];
           r[e] = rn;
           acc += rn * rn;
         });
   }
   double tot;
-  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) sc[out] = ok ? tot : sc[irr];
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    sc[out] = ok ? tot : sc[icur];
+    sc[ialpha] = a;
+  }
 }
 
-// p = r + b p with b = sc[inew]/sc[iold]
-__global__ void __launch_bounds__(KB) k_dcg_p(int64_t n, const double* sc, int inew, int iold,
-                                              const double* __restrict__ r, double* __restrict__ p) {
+__global__ void __launch_bounds__(KB) k_dcg_xp(int64_t n, const double* sc, int ialpha, int inew, int iold,
+                                               const double* __restrict__ r, double* __restrict__ p,
+                                               double* __restrict__ x) {
+  const double a = sc[ialpha];
   const double b = sc[inew] / sc[iold];
-  if ((((uintptr_t)r | (uintptr_t)p) & 15) != 0) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-      p[e] = r[e] + b * p[e];
+  // p lives in a halo window at an odd element offset on some ranks: pairs
+  // only when every operand is 16-byte aligned
+  if ((((uintptr_t)r | (uintptr_t)p | (uintptr_t)x) & 15) != 0) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+      const double pe = p[e];
+      x[e] = x[e] + a * pe;
+      p[e] = r[e] + b * pe;
+    }
     return;
   }
   for_pairs(
       n,
       [&](int64_t e) {
-        const double2 rr = ld2(r + e), pp = ld2(p + e);
+        const double2 rr = ld2(r + e), pp = ld2(p + e), xx = ld2(x + e);
+        st2(x + e, make_double2(xx.x + a * pp.x, xx.y + a * pp.y));
         st2(p + e, make_double2(rr.x + b * pp.x, rr.y + b * pp.y));
       },
-      [&](int64_t e) { p[e] = r[e] + b * p[e]; });
+      [&](int64_t e) {
+        const double pe = p[e];
+        x[e] = x[e] + a * pe;
+        p[e] = r[e] + b * pe;
+      });
 }
 
 // ---------------------------------------------------------------------------
@@ -1715,19 +1729,19 @@ int svb_vec_spmv_dot(svb_vecops* v, const svb_matrix* m, int format, int library
   });
 }
 
-int svb_dcg_update(svb_vecops* v, double* sc, int32_t irr, int32_t ipq, int32_t out, const double* p,
-                   const double* q, double* x, double* r, void* stream) {
+int svb_dcg_rupdate(svb_vecops* v, double* sc, int32_t icur, int32_t ipq, int32_t out, int32_t ialpha,
+                    const double* q, double* r, void* stream) {
   return guard([&] {
-    k_dcg_update<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, irr, ipq, out, p, q, x, r, ptr<double>(v->partials),
-                                                 vctr(v));
+    k_dcg_rupdate<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, icur, ipq, out, ialpha, q, r, ptr<double>(v->partials),
+                                                  vctr(v));
     SVB_CHECK_LAUNCH();
   });
 }
 
-int svb_dcg_p(svb_vecops* v, const double* sc, int32_t inew, int32_t iold, const double* r, double* p,
-              void* stream) {
+int svb_dcg_xp(svb_vecops* v, const double* sc, int32_t ialpha, int32_t inew, int32_t iold, const double* r,
+               double* p, double* x, void* stream) {
   return guard([&] {
-    k_dcg_p<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, inew, iold, r, p);
+    k_dcg_xp<<<v->grid, KB, 0, S(stream)>>>(v->n, sc, ialpha, inew, iold, r, p, x);
     SVB_CHECK_LAUNCH();
   });
 }

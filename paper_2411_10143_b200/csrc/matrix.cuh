@@ -158,7 +158,7 @@ struct RingLayout {
 struct RingDesc {
   int64_t r0, r1, e0, e1;  // rows [r0, r1), entries [e0, e1)
   int poff, coff, voff;    // element offsets of r0 / e0 inside the staged supersets
-  int staged;              // cols (and vals) staged; otherwise read from global
+  int staged;              // entries [e0, e0 + staged) are in shared memory, the rest in global
 };
 
 __device__ __forceinline__ uintptr_t align_dn16(const void* p) { return (uintptr_t)p & ~(uintptr_t)15; }
@@ -166,7 +166,11 @@ __device__ __forceinline__ uintptr_t align_up16(const void* p) {
   return ((uintptr_t)p + 15) & ~(uintptr_t)15;
 }
 
-// One thread: arm `bar` and bulk-copy tile [r0, r1) (entries [e0, e1)) into `stage`.
+// One thread: arm `bar` and bulk-copy tile [r0, r1) (entries [e0, e1)) into
+// `stage`.  The entries are staged up to the stage's capacity: a tile whose
+// entries overflow it keeps its first d->staged entries in shared memory and
+// the readers take the rest from global memory (a power-law tile with one
+// long row no longer drops the whole tile to uncoalesced reads).
 template <class P, int R, int CAP, bool VALS>
 __device__ __forceinline__ void ring_issue(unsigned char* stage, uint64_t* bar, RingDesc* d, int64_t r0, int64_t r1,
                                            int64_t e0, int64_t e1, const P* ptr, const int* cols,
@@ -177,19 +181,21 @@ __device__ __forceinline__ void ring_issue(unsigned char* stage, uint64_t* bar, 
   uint32_t nc = 0, nv = 0;
   uintptr_t ca = 0, va = 0;
   int coff = 0, voff = 0;
+  int64_t nst = 0;
   if (e1 > e0) {
     ca = align_dn16(cols + e0);
-    nc = (uint32_t)(align_up16(cols + e1) - ca);
     coff = (int)(((uintptr_t)(cols + e0) - ca) / 4);
+    nst = e1 - e0;
+    nst = nst < (int64_t)(Lay::SC / 4) - coff ? nst : (int64_t)(Lay::SC / 4) - coff;
     if (VALS) {
       va = align_dn16(vals + e0);
-      nv = (uint32_t)(align_up16(vals + e1) - va);
       voff = (int)(((uintptr_t)(vals + e0) - va) / 8);
+      nst = nst < (int64_t)(Lay::SV / 8) - voff ? nst : (int64_t)(Lay::SV / 8) - voff;
     }
+    nc = (uint32_t)(align_up16(cols + e0 + nst) - ca);
+    if (VALS) nv = (uint32_t)(align_up16(vals + e0 + nst) - va);
   }
-  const bool staged = nc <= Lay::SC && nv <= Lay::SV;
-  if (!staged) nc = nv = 0;
-  *d = RingDesc{r0, r1, e0, e1, (int)(((uintptr_t)(ptr + r0) - pa) / sizeof(P)), coff, voff, staged ? 1 : 0};
+  *d = RingDesc{r0, r1, e0, e1, (int)(((uintptr_t)(ptr + r0) - pa) / sizeof(P)), coff, voff, (int)nst};
   mbar_expect_tx(bar, np + nc + nv);
   bulk_g2s(stage + Lay::SV + Lay::SC, reinterpret_cast<const void*>(pa), np, bar);
   if (nc) bulk_g2s_hint(stage + Lay::SV, reinterpret_cast<const void*>(ca), nc, bar, policy);
@@ -199,18 +205,23 @@ __device__ __forceinline__ void ring_issue(unsigned char* stage, uint64_t* bar, 
 // Diagonal-occupancy bitmap marking with a per-CTA direct-mapped cache of
 // diagonal indices already set: a stencil or banded matrix touches a handful
 // of diagonals, so nearly every entry hits the cache and the global bitmap
-// sees one atomicOr per (CTA, diagonal) instead of one per entry.
+// sees one atomicOr per (CTA, diagonal) instead of one per entry.  D is the
+// diagonal-index type: 32-bit whenever nrows + ncols - 1 < 2^32 (every
+// matrix with int32 columns and at most 2^31 rows), 64-bit otherwise; the
+// empty slot is D(-1), never a valid index.
 constexpr int DIAG_CACHE = 512;
-__device__ __forceinline__ void diag_cache_init(long long* cache) {
-  for (int k = threadIdx.x; k < DIAG_CACHE; k += blockDim.x) cache[k] = -1;
+template <class D>
+__device__ __forceinline__ void diag_cache_init(D* cache) {
+  for (int k = threadIdx.x; k < DIAG_CACHE; k += blockDim.x) cache[k] = D(-1);
 }
-__device__ __forceinline__ void mark_diag(unsigned* __restrict__ bits, long long d, long long* cache) {
+template <class D>
+__device__ __forceinline__ void mark_diag(unsigned* __restrict__ bits, D d, D* cache) {
   const int slot = (int)(d & (DIAG_CACHE - 1));
-  const long long old = *(volatile long long*)(cache + slot);
+  const D old = *(volatile D*)(cache + slot);
   if (old == d) return;
   const unsigned m = 1u << (d & 31);
   unsigned* w = bits + (d >> 5);
-  if (old < 0) {
+  if (old == D(-1)) {
     // first use of the slot (a stencil's few hot diagonals, every CTA at
     // once): test before setting, so the diagonal's word sees reads, not
     // thousands of same-address atomics

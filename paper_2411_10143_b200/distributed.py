@@ -404,12 +404,11 @@ class CudaOps:
         self.gs(self.GS_AXPY, V, k, self._coef, 0, x, x, None, 0)
         self.stream.sync()              # the host coefficient buffer is a temporary
 
-    def cg_update(self, sc, irr: int, ipq: int, out: int, p, q, x, r):
-        _lib.check(self.L.svb_dcg_update(self.h, sc.ptr, irr, ipq, out, p.ptr, q.ptr, x.ptr, r.ptr,
-                                         self.stream.handle))
+    def cg_rupdate(self, sc, icur: int, ipq: int, out: int, ialpha: int, q, r):
+        _lib.check(self.L.svb_dcg_rupdate(self.h, sc.ptr, icur, ipq, out, ialpha, q.ptr, r.ptr, self.stream.handle))
 
-    def cg_p(self, sc, inew: int, iold: int, r, p):
-        _lib.check(self.L.svb_dcg_p(self.h, sc.ptr, inew, iold, r.ptr, p.ptr, self.stream.handle))
+    def cg_xp(self, sc, ialpha: int, inew: int, iold: int, r, p, x):
+        _lib.check(self.L.svb_dcg_xp(self.h, sc.ptr, ialpha, inew, iold, r.ptr, p.ptr, x.ptr, self.stream.handle))
 
     def read_async(self, sc, count: int):
         """Copy sc[:count] into pinned host memory behind the work enqueued so
@@ -826,19 +825,21 @@ def dist_gmres(A: DistOperator, b_local, params) -> dict:
 def dist_cg(A: DistOperator, b_local, params) -> dict:
     """Hestenes-Stiefel CG over row-partitioned vectors (oracle/cpu_oracle.py:
     cg).  Per iteration: one halo exchange + local SpMV with the local p.Ap
-    folded into the same pass (svb_vec_spmv_dot), a fused x/r update with
-    r.r (svb_dcg_update) on device scalars, each followed by an in-place
-    scalar all-reduce, then p = r + beta p
-    (svb_dcg_p).  The host reads (p.Ap, r.r) through pinned memory after the
-    p update is already enqueued, so the GPU keeps working while the host
-    runs the convergence test; a breakdown (p.Ap = 0) leaves x and r
-    untouched, exactly as the unfused loop."""
+    folded into the same pass (svb_vec_spmv_dot), the r update with r.r and
+    alpha kept on the device (svb_dcg_rupdate), each followed by an in-place
+    scalar all-reduce, then x += alpha p and p = r + beta p in one pass
+    (svb_dcg_xp: 24 + 40 instead of 48 + 24 bytes per row).  The host reads
+    (p.Ap, r.r) through pinned memory after the x/p pass is already
+    enqueued, so the GPU keeps working while the host runs the convergence
+    test; a breakdown (p.Ap = 0) stores alpha = 0 and leaves x and r
+    untouched."""
     ops, comm = A.ops, A.comm
     x, r, q, bvec = ops.vec(), ops.vec(), ops.vec(), ops.vec()
     p = ops.vec() if A.no_halo else A.own_view()   # p lives in the halo window
     ops.upload(bvec, b_local) if isinstance(b_local, np.ndarray) else ops.copy(
         ops.view(bvec, 0, ops.n), ops.view(b_local, 0, ops.n))
-    sc = ops.scalars(6)            # [rr_a, rr_b, p.Ap, ||b||^2, true residual, -]
+    IALPHA = 5
+    sc = ops.scalars(6)            # [rr_a, rr_b, p.Ap, ||b||^2, true residual, alpha]
     bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 3))
     hist, done = [], 0
 
@@ -865,10 +866,11 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     while done < params.max_iters:
         A.apply_dot(p, q, sc, 2)              # q = A p with p.q folded into the SpMV pass
         comm.allreduce(sc, 2, 1)
-        ops.cg_update(sc, cur, 2, nxt, p, q, x, r)
+        ops.cg_rupdate(sc, cur, 2, nxt, IALPHA, q, r)
         comm.allreduce(sc, nxt, 1)
         tok = ops.read_async(sc, 3)
-        ops.cg_p(sc, nxt, cur, r, p)         # speculative: unused if the loop stops here
+        ops.cg_xp(sc, IALPHA, nxt, cur, r, p, x)   # x += alpha p; p = r + beta p (the p part is
+                                                   # speculative: unused if the loop stops here)
         vals = ops.read_wait(tok)
         pq, rr_new = float(vals[2]), float(vals[nxt])
         _finite(pq, "curvature p.Ap", done + 1)

@@ -99,6 +99,35 @@ def features_from_aggregates(nrows: int, ncols: int, nnz: int, agg) -> FeatureVe
                          diagfill=diagfill)
 
 
+class CancelEvent(threading.Event):
+    """A threading.Event that also runs registered hooks when it is set (in
+    the setting thread).  The solver's convergence flag is one: a feature
+    pass blocked in native code (svb_features_wait, GIL released) is
+    cancelled by a hook instead of a Python thread polling the event, whose
+    wake-ups every 50 us contend for the GIL with the solver loop."""
+
+    def __init__(self):
+        super().__init__()
+        self._hooks: list = []
+        self._hooks_lock = threading.Lock()
+
+    def add_hook(self, fn) -> None:
+        with self._hooks_lock:
+            self._hooks.append(fn)
+
+    def remove_hook(self, fn) -> None:
+        with self._hooks_lock:
+            if fn in self._hooks:
+                self._hooks.remove(fn)
+
+    def set(self) -> None:
+        super().set()
+        with self._hooks_lock:
+            hooks = list(self._hooks)
+        for fn in hooks:
+            fn()
+
+
 def extract_features(m: CsrMatrix, cancel: threading.Event | None = None, *,
                      counter: TraversalCounter | None = None,
                      row_chunk: int = CANCEL_CHECK_ROWS, stream=None) -> FeatureVector | None:
@@ -120,7 +149,25 @@ def extract_features(m: CsrMatrix, cancel: threading.Event | None = None, *,
     cnt = (ctypes.c_int64 * 2)()
     was = ctypes.c_int32(0)
     try:
-        if cancel is not None:
+        if isinstance(cancel, CancelEvent):
+            # block in native code; a set() from the solver thread forwards
+            # the cancel through the hook (serialised with its retirement)
+            live, lock = [True], threading.Lock()
+
+            def hook():
+                with lock:
+                    if live[0]:
+                        _lib.check(L.svb_features_cancel(job))
+            cancel.add_hook(hook)
+            try:
+                if cancel.is_set():
+                    hook()
+                _lib.check(L.svb_features_wait(job))
+            finally:
+                with lock:
+                    live[0] = False
+                cancel.remove_hook(hook)
+        elif cancel is not None:
             done = ctypes.c_int32(0)
             forwarded = False
             while True:

@@ -59,17 +59,18 @@ class NumpyOps:
     def axpby(self, a, x, b, y):
         y[:] = a * x + b * y
 
-    def cg_update(self, sc, irr, ipq, out, p, q, x, r):
+    def cg_rupdate(self, sc, icur, ipq, out, ialpha, q, r):
         pq = sc[ipq]
-        if pq == 0.0 or not np.isfinite(pq):
-            sc[out] = sc[irr]
-            return
-        a = sc[irr] / pq
-        x += a * p
-        r -= a * q
-        sc[out] = float(np.dot(r, r))
+        ok = pq != 0.0 and np.isfinite(pq)
+        sc[ialpha] = sc[icur] / pq if ok else 0.0
+        if ok:
+            r -= sc[ialpha] * q
+            sc[out] = float(np.dot(r, r))
+        else:
+            sc[out] = sc[icur]
 
-    def cg_p(self, sc, inew, iold, r, p):
+    def cg_xp(self, sc, ialpha, inew, iold, r, p, x):
+        x += sc[ialpha] * p
         p[:] = r + (sc[inew] / sc[iold]) * p
 
     GS_DOT, GS_UPDATE, GS_FINISH, GS_AXPY = 0, 1, 2, 3

@@ -1,6 +1,7 @@
 """GPU parity: device conversions and feature extraction are bit-exact with
 the reference (golden fixtures) and the oracle."""
 import threading
+import time
 
 import numpy as np
 import pytest
@@ -142,6 +143,35 @@ def test_device_cancel_flag_stops_the_pass():
     dia = P.convert(csr, P.FormatTag.DIA)      # from the offsets the pass left on the handle
     want = O.convert(O.OCsr(n, m, ptr, cols, vals), "DIA")
     assert np.array_equal(dia.offsets, want.offsets) and np.array_equal(dia.data, want.data)
+
+
+def test_hooked_cancel_event_stops_a_blocked_pass():
+    """extract_features with the solver's CancelEvent blocks in native code
+    (svb_features_wait); set() from another thread cancels the running pass
+    through the hook, the call returns None, and the handle's next pass is
+    exact (the job was re-armed and recycled)."""
+    torch = pytest.importorskip("torch")
+    from paper_2411_10143_b200 import device
+    from paper_2411_10143_b200.features import CancelEvent
+    n, m, ptr, cols, vals = G.convdiff9(300)
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    s = device.thread_stream()
+    csr._device()
+    for delay in (0.0, 0.005):
+        with torch.cuda.stream(torch.cuda.ExternalStream(s.handle)):
+            torch.cuda._sleep(40_000_000)     # hold the stream ~20 ms
+        ev, box, ctr = CancelEvent(), {}, TraversalCounter()
+        th = threading.Thread(target=lambda: box.setdefault("fv", P.extract_features(csr, ev, counter=ctr,
+                                                                                      stream=s)))
+        th.start()
+        time.sleep(delay)
+        ev.set()
+        th.join(timeout=30)
+        assert not th.is_alive() and box["fv"] is None
+        assert ctr.col_idx_reads < csr.nnz
+        assert not ev._hooks                  # the hook was retired
+    fv = P.extract_features(csr, CancelEvent(), stream=s)
+    assert fv.to_array().tolist() == O.features(O.OCsr(n, m, ptr, cols, vals))
 
 
 def test_device_stencil_generator_matches_host():
