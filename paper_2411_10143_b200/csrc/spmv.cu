@@ -702,6 +702,50 @@ __global__ void __launch_bounds__(256) k_ell_strided(int64_t nrows, int64_t ncol
   }
 }
 
+// The same order with S a compile-time constant (S <= 16, the usual worker
+// counts): the row's columns are swept in increasing k, CH*S at a time with
+// every load issued before the adds (>= 4 columns in flight, as k_ell_sweep),
+// column k added to partial k % S — each partial still sees its columns in
+// increasing k.  (The loop above keeps one load pair in flight per thread:
+// 0.49-0.56 of peak on configs 1-2.)
+template <class T, int S>
+__global__ void __launch_bounds__(256) k_ell_strided_c(int64_t nrows, int64_t ncols, int64_t width,
+                                                       const int* __restrict__ cols, const T* __restrict__ vals,
+                                                       const T* __restrict__ x, T* __restrict__ y) {
+  constexpr int CH = S >= 4 ? 1 : 4 / S;   // S-column chunks per step
+  constexpr int W = CH * S;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T part[S];
+#pragma unroll
+    for (int u = 0; u < S; ++u) part[u] = T(0);
+    int64_t k = 0;
+    for (; k + W <= width; k += W) {
+      T v[W], xv[W];
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        const int c = ld_stream(cols + (k + u) * nrows + i);
+        v[u] = ld_stream(vals + (k + u) * nrows + i);
+        xv[u] = c < ncols ? ld_x(x + c) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < W; ++u) part[u % S] = part[u % S] + v[u] * xv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) {   // tail: k is a multiple of S here
+      if (k + u < width) {
+        const int c = ld_stream(cols + (k + u) * nrows + i);
+        const T v = ld_stream(vals + (k + u) * nrows + i);
+        part[u % S] = part[u % S] + v * (c < ncols ? ld_x(x + c) : T(0));
+      }
+    }
+    T acc = T(0);
+#pragma unroll
+    for (int u = 0; u < S; ++u) acc = acc + part[u];
+    y[i] = acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // DIA/LibA (kernels.py:251-260): thread per row, ascending offsets, cells
 // whose column leaves the matrix are skipped (not added).
@@ -760,38 +804,57 @@ struct DiaOffs {
 };
 constexpr int DIA_REG_MAX = 32;
 
-template <class T, int G, bool DOT>
+// RPT rows per thread (i, i + 256, ...) keeps RPT rows' loads in flight.
+// (Measured for fp32 at config 2: RPT = 4 did not help — the 4-byte
+// requests, not the loads in flight, bound it; see k_dia_f32x4.)
+template <class T, int G, bool DOT, int RPT = 1>
 __global__ void __launch_bounds__(256) k_dia_reg(int64_t nrows, int64_t ncols, int ndiag, DiaOffs offs,
                                                  const T* __restrict__ data, const T* __restrict__ x,
                                                  T* __restrict__ y, const T* __restrict__ dsrc, double* partials,
                                                  unsigned* counter, double* out, const int* skip, int accumulate) {
   if (DOT && skip != nullptr && *skip) return;
   double dot = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    T acc = T(0);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x * RPT + threadIdx.x; i0 < nrows;
+       i0 += (int64_t)gridDim.x * blockDim.x * RPT) {
+    T acc[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) acc[r] = T(0);
     for (int k0 = 0; k0 < ndiag; k0 += G) {
-      T dv[G], xv[G];
+      T dv[G][RPT], xv[G][RPT];
 #pragma unroll
       for (int u = 0; u < G; ++u) {
         const int k = k0 + u;
         if (k < ndiag) {
-          const int64_t j = i + offs.o[k];
-          dv[u] = ld_stream(data + (int64_t)k * nrows + i);
-          xv[u] = (j >= 0 && j < ncols) ? ld_x(x + j) : T(0);
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int64_t i = i0 + r * (int64_t)blockDim.x;
+            const int64_t j = i + offs.o[k];
+            const bool in = i < nrows && j >= 0 && j < ncols;
+            dv[u][r] = i < nrows ? ld_stream(data + (int64_t)k * nrows + i) : T(0);
+            xv[u][r] = in ? ld_x(x + j) : T(0);
+          }
         }
       }
 #pragma unroll
       for (int u = 0; u < G; ++u) {
         const int k = k0 + u;
         if (k < ndiag) {
-          const int64_t j = i + offs.o[k];
-          if (j >= 0 && j < ncols) acc = acc + dv[u] * xv[u];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int64_t j = i0 + r * (int64_t)blockDim.x + offs.o[k];
+            if (j >= 0 && j < ncols) acc[r] = acc[r] + dv[u][r] * xv[u][r];
+          }
         }
       }
     }
-    y[i] = acc;
-    if (DOT) dot = dot + (double)dsrc[i] * (double)acc;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int64_t i = i0 + r * (int64_t)blockDim.x;
+      if (i < nrows) {
+        y[i] = acc[r];
+        if (DOT) dot = dot + (double)dsrc[i] * (double)acc[r];
+      }
+    }
   }
   if (!DOT) return;
   __shared__ double sh[8];
@@ -826,6 +889,62 @@ __global__ void __launch_bounds__(256) k_dia_reg(int64_t nrows, int64_t ncols, i
   }
 }
 
+// fp32 DIA with 16-byte requests: one thread per 4 consecutive rows, the
+// diagonal's data as one float4 (needs nrows % 4 == 0) and x[i+off ..
+// i+off+3] as one float4 when off % 4 == 0, else from the two aligned float4
+// around it (the neighbouring threads' lines: L1 hits).  Row groups whose
+// window leaves [0, ncols) use scalar loads.  Per row the same ascending-
+// diagonal sum as k_dia (skipped cells not added), so y is bit-identical to
+// the scalar fp32 kernel.  (4-byte requests held fp32 DIA at 0.48 of peak on
+// config 2 — slower in absolute time than fp64.)
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float f4_at(const float4& v, int k) {
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+__global__ void __launch_bounds__(256) k_dia_f32x4(int64_t nrows, int64_t ncols, int ndiag, DiaOffs offs,
+                                                   const float* __restrict__ data, const float* __restrict__ x,
+                                                   float* __restrict__ y) {
+  const int64_t ngroups = nrows / 4;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups;
+       gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = gi * 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < ndiag; ++k) {
+      const int64_t off = offs.o[k];
+      const int64_t j = i + off;
+      const float4 dv = ld_stream4(data + (int64_t)k * nrows + i);
+      float xv[4];
+      const int r = (int)(((j % 4) + 4) % 4);
+      const int64_t base = j - r;
+      if (base >= 0 && base + 8 <= ncols) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(x + base));
+        if (r == 0) {
+          xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+        } else {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(x + base + 4));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xv[u] = r + u < 4 ? f4_at(a, r + u) : f4_at(b, r + u - 4);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = acc[u] + f4_at(dv, u) * xv[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t ju = j + u;
+          if (ju >= 0 && ju < ncols) acc[u] = acc[u] + f4_at(dv, u) * __ldg(x + ju);
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(y + i) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
 // Grid of a grid-stride kernel sized by its real occupancy: grid_for()'s
 // 8 CTAs/SM assumes <= 32 registers; a kernel that fits fewer would leave a
 // partial second wave doing a full share of the rows (measured: the fused
@@ -856,18 +975,24 @@ static bool dia_reg_enabled() {
   return on;
 }
 
+static bool launch_dia_f32x4(const svb_matrix* m, const float* vals, const float* x, float* y, cudaStream_t s);
+
 template <class T, bool DOT>
 static bool launch_dia_reg(const svb_matrix* m, const T* vals, const T* x, T* y, const T* dsrc, double* partials,
                            unsigned* counter, double* out, const int* skip, int accumulate, unsigned max_grid,
                            cudaStream_t s) {
   if (!dia_reg_enabled() || m->ndiag < 1 || m->ndiag > DIA_REG_MAX || m->h_offs.size() != (size_t)m->ndiag)
     return false;
-  const unsigned g = resident_grid((const void*)k_dia_reg<T, 3, DOT>, 256, m->nrows);
+  if constexpr (std::is_same<T, float>::value && !DOT) {
+    if (launch_dia_f32x4(m, vals, x, y, s)) return true;
+  }
+  constexpr int RPT = 1;
+  const unsigned g = resident_grid((const void*)k_dia_reg<T, 3, DOT, RPT>, 256, (m->nrows + RPT - 1) / RPT);
   if (DOT && g > max_grid) return false;
   DiaOffs o{};
   for (int k = 0; k < m->ndiag; ++k) o.o[k] = m->h_offs[k];
-  k_dia_reg<T, 3, DOT><<<g, 256, 0, s>>>(m->nrows, m->ncols, (int)m->ndiag, o, vals, x, y, dsrc, partials, counter,
-                                         out, skip, accumulate);
+  k_dia_reg<T, 3, DOT, RPT><<<g, 256, 0, s>>>(m->nrows, m->ncols, (int)m->ndiag, o, vals, x, y, dsrc, partials,
+                                              counter, out, skip, accumulate);
   return true;
 }
 
@@ -939,6 +1064,15 @@ __global__ void __launch_bounds__(256) k_dia_dot(int64_t nrows, int64_t ncols, i
     *out = accumulate ? *out + g : g;
     *counter = 0;
   }
+}
+
+static bool launch_dia_f32x4(const svb_matrix* m, const float* vals, const float* x, float* y, cudaStream_t s) {
+  if (m->nrows % 4 != 0 || m->nrows < 4 || (((uintptr_t)vals | (uintptr_t)x | (uintptr_t)y) & 15) != 0) return false;
+  const unsigned g = resident_grid((const void*)k_dia_f32x4, 256, m->nrows / 4);
+  DiaOffs o{};
+  for (int k = 0; k < m->ndiag; ++k) o.o[k] = m->h_offs[k];
+  k_dia_f32x4<<<g, 256, 0, s>>>(m->nrows, m->ncols, (int)m->ndiag, o, vals, x, y);
+  return true;
 }
 
 void launch_dia_dot(const svb_matrix* m, const double* x, double* y, const double* dsrc, double* partials,
@@ -1266,8 +1400,25 @@ static void launch_spmv(const svb_matrix* m, int fmt, int lib, int lane, int wor
       k_ell_sweep<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, ptr<int>(m->cols), vals, x, y);
     else {
       const int S = (int)std::min<int64_t>(workers, m->width);
-      k_ell_strided<T><<<grid_for(n, 256, 8), 256, 0, s>>>(n, m->ncols, m->width, S, ptr<int>(m->cols),
-                                                           vals, x, y);
+      const unsigned g = grid_for(n, 256, 8);
+      const int* ec = ptr<int>(m->cols);
+      // S >= width: one column per partial, i.e. the plain column sweep's
+      // sums (0 + p is p; the partials start from +0.0)
+      if (S >= m->width) {
+        k_ell_sweep<T><<<g, 256, 0, s>>>(n, m->ncols, m->width, ec, vals, x, y);
+      } else {
+        switch (S) {
+#define SVB_ELLC(K) \
+  case K:           \
+    k_ell_strided_c<T, K><<<g, 256, 0, s>>>(n, m->ncols, m->width, ec, vals, x, y); \
+    break;
+          SVB_ELLC(1) SVB_ELLC(2) SVB_ELLC(3) SVB_ELLC(4) SVB_ELLC(5) SVB_ELLC(6) SVB_ELLC(7) SVB_ELLC(8)
+          SVB_ELLC(9) SVB_ELLC(10) SVB_ELLC(11) SVB_ELLC(12) SVB_ELLC(13) SVB_ELLC(14) SVB_ELLC(15) SVB_ELLC(16)
+#undef SVB_ELLC
+          default: k_ell_strided<T><<<g, 256, 0, s>>>(n, m->ncols, m->width, S, ec, vals, x, y);
+        }
+      }
+
     }
   } else if (fmt == SVB_DIA) {
     if (!launch_dia_reg<T, false>(m, vals, x, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, s))

@@ -26,19 +26,23 @@ PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
     if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
 
 
+F32 = os.environ.get("SWEEP_DTYPE", "f64") == "f32"   # fp32 values, x and y (north star: fp64/fp32)
+
+
 def alg_bytes(fmt, rep, n, ncols, lib=""):
     inf = rep._device().info
+    v = 4 if F32 else 8                 # value / vector element bytes
     if fmt == "CSR":
-        return 12 * inf.nnz + 4 * (n + 1) + 8 * ncols + 8 * n
+        return (4 + v) * inf.nnz + 4 * (n + 1) + v * ncols + v * n
     if fmt == "COO" and lib == "LibA":
-        return 12 * inf.nnz + 8 * (n + 1) + 8 * ncols + 8 * n
+        return (4 + v) * inf.nnz + 8 * (n + 1) + v * ncols + v * n
     if fmt == "COO":
-        return 16 * inf.nnz + 8 * ncols + 8 * n
+        return (8 + v) * inf.nnz + v * ncols + v * n
     if fmt == "ELL":
-        return 12 * n * inf.width + 8 * ncols + 8 * n
+        return (4 + v) * n * inf.width + v * ncols + v * n
     if fmt == "DIA":
-        return 8 * inf.ndiag * n + 8 * ncols + 8 * n
-    return 12 * n * inf.width + 16 * inf.spill_nnz + 8 * ncols + 16 * n
+        return v * inf.ndiag * n + v * ncols + v * n
+    return (4 + v) * n * inf.width + (8 + v) * inf.spill_nnz + v * ncols + 2 * v * n
 
 
 def stencil(kind):
@@ -62,11 +66,12 @@ def main():
     mats = {build[w][0]: build[w][1]() for w in which}
     s = device.thread_stream()
     ext = torch.cuda.ExternalStream(s.handle)
-    out = {"peak_gbs": PEAK, "runs": RUNS, "results": {}}
+    out = {"peak_gbs": PEAK, "runs": RUNS, "dtype": "f32" if F32 else "f64", "results": {}}
     for name, A in mats.items():
         n = A.nrows
-        x = device.DeviceVector.from_numpy(np.random.default_rng(0).uniform(0.5, 1.5, n), s)
-        y = device.DeviceVector(n)
+        xh = np.random.default_rng(0).uniform(0.5, 1.5, n)
+        x = device.DeviceVector.from_numpy(xh.astype(np.float32) if F32 else xh, s)
+        y = device.DeviceVector(n, np.float32) if F32 else device.DeviceVector(n)
         res = {}
         reps = {}
         only = os.environ.get("SWEEP_TOKENS")
@@ -84,11 +89,11 @@ def main():
             if rep is None:
                 continue
             for _ in range(3):
-                launch(cfg, rep, x.ptr, y.ptr, workers=4, stream=s)
+                launch(cfg, rep, x.ptr, y.ptr, workers=4, f32=F32, stream=s)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ext)
             for _ in range(RUNS):
-                launch(cfg, rep, x.ptr, y.ptr, workers=4, stream=s)
+                launch(cfg, rep, x.ptr, y.ptr, workers=4, f32=F32, stream=s)
             e1.record(ext)
             e1.synchronize()
             us = e0.elapsed_time(e1) / RUNS * 1e3

@@ -62,6 +62,8 @@ def matrix(name: str):
         return G.convdiff9(2000)
     if name == "config3":
         return G.powerlaw_spd(8_000_000, seed=0)
+    if name == "config5_120":
+        return G.laplace27(120)     # config 5's matrix family at 120^3 (600^3 has 5.8 B nnz)
     raise KeyError(name)
 
 
@@ -113,7 +115,8 @@ def build(name: str, models) -> dict:
     csr = S.CsrMatrix(n, m, ptr, cols, vals)
     x = np.random.default_rng(0).uniform(0.5, 1.5, size=m)
     doc["spmv_reference_sha256"] = sha(S.spmv_reference(csr, x))
-    doc["spmv"] = spmv_hashes(csr, x, skip=("ELL", "DIA") if name == "config3" else ())
+    doc["spmv"] = spmv_hashes(csr, x, skip=("ELL", "DIA") if name == "config3" else
+                              ("COO", "ELL", "HYB") if name == "config5_120" else ())
     fv = S.extract_features(csr)
     doc["features"] = [float(v) for v in fv.to_array()]
     stages = []
@@ -135,6 +138,15 @@ def build(name: str, models) -> dict:
     elif name == "config3":
         b = np.random.default_rng(0).standard_normal(n)      # rhs="random", seed 0 (solver.py:190-191)
         doc["cg"] = cg_oracle(csr, "CSR/LibB", b)
+    elif name == "config5_120":
+        # the bench's predict-then-solve CG (b = A*1, the cascade's kernel)
+        b = S.spmv_reference(csr, np.ones(n))
+        doc["cg"] = cg_oracle(csr, final.token(), b)
+        dia = S.convert(csr, S.FormatTag.DIA)
+        r = O.cg(lambda v: S.execute_spmv(S.SpmvConfig(S.FormatTag.DIA, S.Library.LIB_A), dia, v, workers=4), b,
+                 tol=1e-8, max_iters=20000)
+        doc["cg"]["x_norm"] = float(np.linalg.norm(r["x"]))
+        doc["cg"]["x_head"] = [float(v) for v in r["x"][:4]]
     doc["seconds"] = time.perf_counter() - t0
     return doc
 

@@ -64,10 +64,13 @@ def matrix(name):
         return P.CsrMatrix.stencil((2000, 2000), offs, w)
     if name == "config3":
         return G.powerlaw_spd_device(8_000_000, seed=0)
+    if name == "config5_120":       # config 5's 27-point Laplacian family at 120^3
+        offs, w = stencil_offsets(3, 26.0, lambda o: -1.0)
+        return P.CsrMatrix.stencil((120, 120, 120), offs, w)
     raise KeyError(name)
 
 
-CONFIGS = ["config1", "config2", "config3"]
+CONFIGS = ["config1", "config2", "config3", "config5_120"]
 
 
 @pytest.mark.parametrize("name", CONFIGS)
@@ -101,7 +104,8 @@ def test_every_spmv_configuration_bit_exact_at_scale(name):
         else:
             assert sha(y) == want["sha256"], cfg.token()
         checked += 1
-    assert checked >= (10 if name == "config3" else 13)
+    assert checked == sum(1 for v in f["spmv"].values() if "inapplicable" not in v)
+    assert checked >= (8 if name == "config5_120" else 10 if name == "config3" else 13)
 
 
 @pytest.mark.parametrize("name", CONFIGS)
@@ -242,3 +246,43 @@ def test_int64_row_pointers_on_the_golden_cases():
                          env=env, capture_output=True, text=True, timeout=1200, cwd=str(ROOT))
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert " passed" in out.stdout and "failed" not in out.stdout
+
+
+def test_config5_family_row_partitioned_cg_matches_reference():
+    """The bench's path (device-generated slab, exact global features ->
+    shipped cascade -> DIA, row-partitioned CG over NCCL at world 1) on
+    config 5's matrix family at 120^3 against the reference-driven fixture:
+    same kernel choice, iterations within 1, residual <= tol, same x."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_10143_b200.distributed import distributed_stencil_solve
+    f = fixtures()["config5_120"]
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        offs, w = stencil_offsets(3, 26.0, lambda o: -1.0)
+        params = P.GmresParams(tol=1e-8, max_iters=20000)
+        res, blk = distributed_stencil_solve("cg", (120, 120, 120), offs, w, params,
+                                             models=P.CascadeModelSet.load_dir(MODELS))
+        assert sha(np.asarray(blk._dev_csr.row_ptr, np.int64), np.asarray(blk._dev_csr.col_idx, np.int64),
+                   blk._dev_csr.values) == f["csr_sha256"]
+        assert res["config"] == f["cascade"]["final"]
+        assert res["converged"] and res["final"] <= 1e-8
+        assert abs(res["iterations"] - f["cg"]["iterations"]) <= 1
+        x = res["x"].to_numpy()
+        # two CG runs with different dot-product orders, both stopped at
+        # relative residual <= 1e-8: x agrees to the solve's own accuracy
+        assert abs(np.linalg.norm(x) - f["cg"]["x_norm"]) <= 1e-8 * f["cg"]["x_norm"]
+        assert np.allclose(x[:4], f["cg"]["x_head"], rtol=1e-7, atol=0)
+        assert np.allclose(res["history"][:5], f["cg"]["history_head"], rtol=1e-9, atol=0)
+    finally:
+        dist.destroy_process_group()

@@ -135,6 +135,45 @@ def test_dia_staged_kernel_bit_exact(n, offsets):
     assert rel(y32.astype(np.float64), want) <= FP32_TOL
 
 
+def test_ell_strided_every_stride_bit_exact():
+    """ELL/LibC with S = min(workers, width) from 1 to past the width: the
+    compile-time-S kernels (S <= 16), the S >= width column sweep and the
+    generic loop (S > 16) all reproduce the reference's strided partials."""
+    n, m, ptr, cols, vals = G.banded(12_000, list(range(-11, 12)), seed=3, diagonal_boost=4.0)   # width 23
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    ell = P.convert(csr, P.FormatTag.ELL)
+    oell = O.convert(O.OCsr(n, m, ptr, cols, vals), "ELL")
+    cfg = P.SpmvConfig(P.FormatTag.ELL, P.Library.LIB_C)
+    x = np.random.default_rng(9).uniform(-1.0, 1.0, size=m)
+    assert ell.width == 23
+    for w in list(range(1, 19)) + [22, 23, 24, 64]:
+        assert np.array_equal(P.execute_spmv(cfg, ell, x, workers=w), O.spmv("ELL/LibC", oell, x, workers=w)), w
+
+
+@pytest.mark.parametrize("n,offsets", [
+    (40_000, [-201, -200, -199, -1, 0, 1, 199, 200, 201]),   # every offset residue mod 4
+    (40_004, [-3, -2, -1, 0, 1, 2, 3]),
+    (4_096, [-4095, -5, 0, 6, 4095]),                         # corners: the scalar edge path
+    (40_001, [-7, 0, 7])])                                    # nrows % 4 != 0: the scalar kernel
+def test_fp32_dia_bit_exact_against_float32_sweep(n, offsets):
+    """fp32 DIA (k_dia_f32x4: 16-byte requests, four rows per thread) against
+    the reference's diagonal sweep evaluated in float32 (each product and sum
+    rounded to fp32, ascending offsets, out-of-range cells skipped)."""
+    nn, m, ptr, cols, vals = G.banded(n, offsets, seed=n, diagonal_boost=2.0)
+    dia = P.convert(P.CsrMatrix(nn, m, ptr, cols, vals), P.FormatTag.DIA)
+    x32 = np.random.default_rng(n).uniform(-1.0, 1.0, size=m).astype(np.float32)
+    data32 = np.asarray(dia.data).astype(np.float32)
+    want = np.zeros(nn, dtype=np.float32)
+    for k, off in enumerate(np.asarray(dia.offsets).tolist()):
+        i0, i1 = max(0, -off), min(nn, m - off)
+        if i0 < i1:
+            want[i0:i1] = want[i0:i1] + data32[k, i0:i1] * x32[i0 + off:i1 + off]
+    s = device.thread_stream()
+    y32 = P.execute_spmv(P.SpmvConfig(P.FormatTag.DIA, P.Library.LIB_A), dia,
+                         device.DeviceVector.from_numpy(x32, s), stream=s).to_numpy(s)
+    assert y32.dtype == np.float32 and np.array_equal(y32, want)
+
+
 def test_ptr64_mode_is_what_the_environment_asks():
     """tests/test_gpu_scale.py re-runs this module with SPMVTUNE_FORCE_PTR64=1:
     the int64 row-pointer kernels must then really be the ones running."""
