@@ -428,6 +428,35 @@ int svb_cg_run(const svb_matrix* A, svb_config cfg, const double* b_dev, double*
                svb_swap* timeline_host, int32_t timeline_cap, svb_solve_report* out);
 
 
+/* ---- peer-memory collectives (csrc/peer.cu; distributed.py PeerComm) ----
+ * The row-partitioned CG's per-iteration exchanges done by the solver's own
+ * kernels over NVLink/NVSwitch peer memory instead of NCCL: an all-reduce
+ * of <= 64 device doubles through per-rank mailboxes (every rank stores its
+ * values into every mailbox, release-tags them, sums its own mailbox in rank
+ * order: bit-identical on all ranks), and the halo pushed by the x/p pass
+ * straight into the neighbours' windows with a release tag the neighbour's
+ * boundary SpMV waits for (svb_peer_wait_halo).  Mailboxes and windows are
+ * cudaMalloc'd (CUDA IPC exportable: svb_peer_ipc_handle/open); every wait
+ * has a 30 s deadline that raises svb_peer_error instead of hanging.
+ * Replaces the NCCL calls of the reference-shaped loop (oracle/cpu_oracle.py:cg;
+ * the reference itself has no distributed solver). */
+typedef struct svb_peer svb_peer;
+int svb_peer_create(int rank, int world, svb_peer** out);
+int svb_peer_destroy(svb_peer* g);
+int svb_peer_mailbox(const svb_peer* g, void** dev_ptr);
+int svb_peer_set_mailbox(svb_peer* g, int rank, void* dev_ptr);
+int svb_peer_alloc(int64_t bytes, void** out);
+int svb_peer_free(void* dev_ptr);
+int svb_peer_ipc_handle(void* dev_ptr, void* handle64);
+int svb_peer_ipc_open(const void* handle64, void** dev_ptr);
+int svb_peer_ipc_close(void* dev_ptr);
+int svb_peer_error(const svb_peer* g, int* err);
+int svb_peer_allreduce(svb_peer* g, double* v_dev, int count, void* stream);
+int svb_peer_wait_halo(svb_peer* g, const int32_t* peers, int npeers, void* stream);
+int svb_dcg_xp_push(svb_peer* g, int64_t n, const double* sc_dev, int32_t ialpha, int32_t inew, int32_t iold,
+                    const double* r_dev, double* p_dev, double* x_dev, int nseg, const int64_t* lo,
+                    const int64_t* cnt, double* const* dst_dev, const int32_t* peer, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,19 @@ _SIGS = {
     "svb_coo_from_triplets": [C.c_int64, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, _P, _PP],
     "svb_event_sync": [_P],
     "svb_dcg_rupdate": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "svb_peer_create": [C.c_int, C.c_int, C.POINTER(C.c_void_p)],
+    "svb_peer_destroy": [_P],
+    "svb_peer_mailbox": [_P, C.POINTER(C.c_void_p)],
+    "svb_peer_set_mailbox": [_P, C.c_int, _P],
+    "svb_peer_alloc": [C.c_int64, C.POINTER(C.c_void_p)],
+    "svb_peer_free": [_P],
+    "svb_peer_ipc_handle": [_P, _P],
+    "svb_peer_ipc_open": [_P, C.POINTER(C.c_void_p)],
+    "svb_peer_ipc_close": [_P],
+    "svb_peer_error": [_P, C.POINTER(C.c_int)],
+    "svb_peer_allreduce": [_P, _P, C.c_int, _P],
+    "svb_peer_wait_halo": [_P, _P, C.c_int, _P],
+    "svb_dcg_xp_push": [_P, C.c_int64, _P, _I32, _I32, _I32, _P, _P, _P, C.c_int, _P, _P, _P, _P, _P],
     "svb_dcg_xp": [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "svb_cg_step_batched_dia": [_P, _P, C.c_double, _P],
     "svb_krylov_mark": [_P, _P],

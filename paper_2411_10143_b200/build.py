@@ -37,6 +37,7 @@ SOURCES = {
     "forest.cpp": [],
     "mmio.cu": [],
     "driver.cu": [],
+    "peer.cu": [],
 }
 
 

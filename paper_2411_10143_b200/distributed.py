@@ -41,7 +41,7 @@ from .kernels import Library, SpmvConfig, default_workers, launch
 __all__ = ["partition_rows", "LocalBlock", "local_block", "HaloPlan", "DistOperator", "CudaOps",
            "NcclComm", "HostStagedComm", "interior_rows", "dist_gmres", "dist_cg", "global_features", "distributed_solve",
            "stencil_partition", "stencil_block_window", "stencil_block", "distributed_stencil_solve",
-           "slab_block", "device_diag_offsets", "distributed_solve_slab"]
+           "slab_block", "device_diag_offsets", "distributed_solve_slab", "PeerComm", "peer_comm_or_base"]
 
 
 # ---------------------------------------------------------------------------
@@ -592,6 +592,181 @@ class HostStagedComm:
             self._up(v.ptr, t.numpy())
 
 
+class _PeerBuffer:
+    """A cudaMalloc'd float64 buffer (svb_peer_alloc): CUDA-IPC exportable, so
+    other ranks' kernels can store into it (the halo windows)."""
+
+    def __init__(self, n: int):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().svb_peer_alloc(8 * int(n), ctypes.byref(h)))
+        self.ptr, self.n, self.nbytes = int(h.value), int(n), 8 * int(n)
+
+    def __del__(self):
+        ptr, self.ptr = getattr(self, "ptr", 0), 0
+        if ptr:
+            try:
+                _lib.load().svb_peer_free(ptr)
+            except Exception:
+                pass
+
+
+class PeerComm:
+    """Collectives done by this package's own kernels over NVLink / NVSwitch
+    peer memory (csrc/peer.cu) on top of a base comm (NcclComm, or
+    HostStagedComm in the one-GPU tests):
+
+    * ``allreduce`` of up to 64 device doubles through the per-rank
+      mailboxes (k_peer_allreduce, one tiny kernel on the solver stream, no
+      host involvement; bit-identical totals on every rank);
+    * the CG loop's halo: the x/p pass pushes the rows each neighbour needs
+      straight into the neighbour's window (svb_dcg_xp_push) and the
+      neighbour's boundary SpMV waits on the device for the tag
+      (svb_peer_wait_halo) — ``DistOperator.setup_push`` builds the plan;
+    * everything else (general halo exchanges, object gathers, max
+      all-reduces, all-reduces above 64 doubles) goes to the base comm.
+
+    ``ipc``: exchange CUDA IPC handles (one process per GPU); otherwise the
+    ranks share one address space and exchange raw device pointers.  Setup
+    is collective and fails on every rank together (``PeerSetupError``), so
+    callers can fall back to the base comm without desynchronising."""
+
+    MAXC = 64
+
+    class PeerSetupError(RuntimeError):
+        pass
+
+    def __init__(self, base, stream: device.Stream, ipc: bool = True):
+        self.base, self.stream, self.ipc = base, stream, bool(ipc)
+        self.rank, self.world = base.rank, base.world
+        self.L = _lib.lib()
+        self.h = None
+        self._opened: list[int] = []
+        ok, err, mb = True, "", None
+        try:
+            h = ctypes.c_void_p()
+            _lib.check(self.L.svb_peer_create(self.rank, self.world, ctypes.byref(h)))
+            self.h = h.value
+            mbp = ctypes.c_void_p()
+            _lib.check(self.L.svb_peer_mailbox(self.h, ctypes.byref(mbp)))
+            mb = int(mbp.value)
+        except Exception as exc:   # noqa: BLE001 — reported collectively below
+            ok, err = False, f"{type(exc).__name__}: {exc}"
+        ptrs = self._share(mb, ok, err)
+        for q, ptr in enumerate(ptrs):
+            _lib.check(self.L.svb_peer_set_mailbox(self.h, q, ptr))
+
+    # -- collective pointer sharing (every step ends in an all-gather, so a
+    # failure on one rank is seen by all of them at the same point)
+    def _export(self, ptr: int):
+        if not self.ipc:
+            return ptr
+        buf = (ctypes.c_char * 64)()
+        _lib.check(self.L.svb_peer_ipc_handle(ptr, buf))
+        return bytes(buf)
+
+    def _share(self, ptr: int | None, ok: bool = True, err: str = "") -> list[int]:
+        token = None
+        if ok:
+            try:
+                token = self._export(ptr)
+            except Exception as exc:   # noqa: BLE001
+                ok, err = False, f"{type(exc).__name__}: {exc}"
+        got = self.base.allgather_obj((ok, err, token))
+        bad = [e for o, e, _ in got if not o]
+        if bad:
+            raise PeerComm.PeerSetupError(f"peer setup failed on {len(bad)} rank(s): {bad[0]}")
+        out, ok, err = [], True, ""
+        for q, (_, _, tok) in enumerate(got):
+            if q == self.rank or not self.ipc:
+                out.append(ptr if q == self.rank else int(tok))
+                continue
+            try:
+                d = ctypes.c_void_p()
+                _lib.check(self.L.svb_peer_ipc_open(ctypes.c_char_p(tok), ctypes.byref(d)))
+                self._opened.append(int(d.value))
+                out.append(int(d.value))
+            except Exception as exc:   # noqa: BLE001
+                ok, err = False, f"{type(exc).__name__}: {exc}"
+                out.append(0)
+        fails = [e for o, e in self.base.allgather_obj((ok, err)) if not o]
+        if fails:
+            raise PeerComm.PeerSetupError(f"peer mapping failed on {len(fails)} rank(s): {fails[0]}")
+        return out
+
+    def alloc(self, n: int) -> _PeerBuffer:
+        return _PeerBuffer(n)
+
+    def share_buffer(self, buf) -> list[int]:
+        """Every rank's ``buf`` (same call on all ranks) as addressable here."""
+        return self._share(int(buf.ptr))
+
+    def check(self):
+        e = ctypes.c_int(0)
+        _lib.check(self.L.svb_peer_error(self.h, ctypes.byref(e)))
+        if e.value:
+            raise RuntimeError("peer collective timed out (a rank stopped participating)")
+
+    # -- collectives
+    def allreduce(self, sc, first: int, count: int):
+        if count > self.MAXC:
+            return self.base.allreduce(sc, first, count)
+        _lib.check(self.L.svb_peer_allreduce(self.h, sc.ptr + 8 * first, int(count), self.stream.handle))
+
+    def allreduce_max(self, arr):
+        return self.base.allreduce_max(arr)
+
+    def allgather_obj(self, obj):
+        return self.base.allgather_obj(obj)
+
+    def exchange(self, sends, recvs):
+        self.base.exchange(sends, recvs)
+
+    def exchange_start(self, sends, recvs):
+        return self.base.exchange_start(sends, recvs)
+
+    def exchange_finish(self, token):
+        self.base.exchange_finish(token)
+
+    def wait_halo(self, peers):
+        arr = (ctypes.c_int32 * max(1, len(peers)))(*peers)
+        _lib.check(self.L.svb_peer_wait_halo(self.h, arr, len(peers), self.stream.handle))
+
+    def xp_push(self, n: int, sc, ialpha: int, inew: int, iold: int, r, p, x, segs):
+        k = len(segs)
+        lo = (ctypes.c_int64 * 2)(*[sg[0] for sg in segs])
+        cnt = (ctypes.c_int64 * 2)(*[sg[1] for sg in segs])
+        dst = (ctypes.c_void_p * 2)(*[sg[2] for sg in segs])
+        peer = (ctypes.c_int32 * 2)(*[sg[3] for sg in segs])
+        _lib.check(self.L.svb_dcg_xp_push(self.h, int(n), sc.ptr, ialpha, inew, iold, r.ptr, p.ptr, x.ptr, k,
+                                          lo, cnt, dst, peer, self.stream.handle))
+
+    def close(self):
+        """Collective: unmap the peers' buffers after everyone is done."""
+        if self.h is None:
+            return
+        self.stream.sync()
+        self.base.allgather_obj(None)
+        for d in self._opened:
+            self.L.svb_peer_ipc_close(d)
+        self._opened = []
+        self.base.allgather_obj(None)
+        self.L.svb_peer_destroy(self.h)
+        self.h = None
+
+
+def peer_comm_or_base(base, stream: device.Stream, ipc: bool = True):
+    """PeerComm over ``base`` unless SPMVTUNE_P2P=0, one rank, or the
+    collective setup fails (then the base comm, on every rank)."""
+    if os.environ.get("SPMVTUNE_P2P", "1") == "0" or base.world == 1:
+        return base
+    try:
+        return PeerComm(base, stream, ipc=ipc)
+    except PeerComm.PeerSetupError as exc:
+        import warnings
+        warnings.warn(f"peer-memory collectives unavailable, using {type(base).__name__}: {exc}")
+        return base
+
+
 # ---------------------------------------------------------------------------
 # distributed operator: halo exchange + local SpMV
 # ---------------------------------------------------------------------------
@@ -600,7 +775,10 @@ class DistOperator:
         self.block, self.comm, self.ops, self.cfg = block, comm, ops, cfg
         windows = comm.allgather_obj((block.cmin, block.cmax))
         self.plan = HaloPlan.build(bounds, windows, comm.rank)
-        self.window = ops.vec(block.window)
+        self._windows = windows
+        # a window other ranks push into must be peer-mappable
+        self.window = comm.alloc(block.window) if hasattr(comm, "alloc") else ops.vec(block.window)
+        self.push = None
         self.own = block.r0 - block.cmin
         # no halo: the window is exactly this rank's rows (one rank, or a
         # block-diagonal matrix), so the SpMV reads the source vector itself
@@ -627,6 +805,51 @@ class DistOperator:
     def swap(self, cfg: SpmvConfig):
         self.cfg = cfg
         self._prepare(cfg)
+
+    def setup_push(self) -> bool:
+        """Collective: map every rank's window and build this rank's halo-push
+        segments (local rows [lo, lo+cnt) -> peer window address) for
+        PeerComm's x/p pass.  False on every rank unless all can push (<= 2
+        neighbours each way, the vector kept in the window)."""
+        comm, b = self.comm, self.block
+        if not hasattr(comm, "share_buffer"):
+            return False
+        ptrs = comm.share_buffer(self.window)
+        segs = [(lo - b.r0, hi - lo, ptrs[p] + 8 * (lo - self._windows[p][0]), p)
+                for p, lo, hi in self.plan.sends if hi > lo]
+        peers = [p for p, lo, hi in self.plan.recvs if hi > lo]
+        mine = len(segs) <= 2 and len(peers) <= 2
+        if not all(comm.allgather_obj(mine)):
+            return False
+        self.push = (segs, peers)
+        return True
+
+    def apply_dot_pushed(self, src, dst, sc, slot: int):
+        """apply_dot when the halo was pushed into this rank's window by the
+        neighbours' last x/p pass: the interior rows run at once, the stream
+        then waits on the device for the neighbours' tags, then the boundary
+        rows.  ``src`` must be the window's own slice (CG's p)."""
+        ops = self.ops
+        _, peers = self.push
+        fused = hasattr(ops, "spmv_dot")
+
+        def part(mat, d, sv, acc):
+            if fused:
+                ops.spmv_dot(mat, self.cfg, self.window, d, sv, sc, slot, acc)
+            else:
+                ops.spmv(mat, self.cfg, self.window, d)
+        if self.parts is None:
+            self.comm.wait_halo(peers)
+            part(self.mat, dst, src, False)
+        else:
+            for k, (a, cnt, mat) in enumerate(self.parts):
+                if k == 1:
+                    self.comm.wait_halo(peers)
+                part(mat, ops.view(dst, a, cnt), ops.view(src, a, cnt), k > 0)
+            if len(self.parts) == 1:
+                self.comm.wait_halo(peers)
+        if not fused:
+            ops.dot(src, dst, sc, slot)
 
     def own_view(self):
         """This rank's slice of the window buffer: a vector kept there (CG's
@@ -842,10 +1065,11 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     sc = ops.scalars(6)            # [rr_a, rr_b, p.Ap, ||b||^2, true residual, alpha]
     bnorm = math.sqrt(_global_norm2(ops, comm, bvec, sc, 3))
     hist, done = [], 0
+    push = False                   # halo pushed by the x/p pass (PeerComm), set below
 
     def out(conv, fin, status="ok"):
         return {"converged": conv, "iterations": done, "history": hist, "x": x, "final": fin,
-                "status": status}
+                "status": status, "halo_push": push}
 
     def true_res() -> float:
         A.apply(x, q)
@@ -863,15 +1087,30 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     ops.axpby(1.0, r, 0.0, p)
     cur, nxt = 0, 1
     _global_norm2(ops, comm, r, sc, cur)
+    # peer-memory mode (PeerComm): the x/p pass pushes the next direction's
+    # halo into the neighbours' windows, the next SpMV waits for it on the
+    # device — no exchange call in the loop
+    push = (not A.no_halo) and A.setup_push()
+    pushed = False
     while done < params.max_iters:
-        A.apply_dot(p, q, sc, 2)              # q = A p with p.q folded into the SpMV pass
+        if pushed:
+            A.apply_dot_pushed(p, q, sc, 2)
+        else:
+            A.apply_dot(p, q, sc, 2)          # q = A p with p.q folded into the SpMV pass
         comm.allreduce(sc, 2, 1)
         ops.cg_rupdate(sc, cur, 2, nxt, IALPHA, q, r)
         comm.allreduce(sc, nxt, 1)
         tok = ops.read_async(sc, 3)
-        ops.cg_xp(sc, IALPHA, nxt, cur, r, p, x)   # x += alpha p; p = r + beta p (the p part is
-                                                   # speculative: unused if the loop stops here)
+        # x += alpha p; p = r + beta p (the p part is speculative: unused if
+        # the loop stops here)
+        if push:
+            comm.xp_push(ops.n, sc, IALPHA, nxt, cur, r, p, x, A.push[0])
+            pushed = True
+        else:
+            ops.cg_xp(sc, IALPHA, nxt, cur, r, p, x)
         vals = ops.read_wait(tok)
+        if push or hasattr(comm, "check"):
+            comm.check()                      # a timed-out peer wait raises here, not as bad numbers
         pq, rr_new = float(vals[2]), float(vals[nxt])
         _finite(pq, "curvature p.Ap", done + 1)
         if pq == 0.0:
@@ -891,6 +1130,7 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
                 return out(True, fin)
             ops.axpby(1.0, r, 0.0, p)
             _global_norm2(ops, comm, r, sc, cur)
+            pushed = False                        # the restart's p goes out by exchange
             continue
     fin = true_res()
     return out(fin <= params.tol, fin)
@@ -936,7 +1176,7 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
     if blk is None:
         blk = stencil_block(dims, offsets, weights, r0, r1, stream)
     n = blk.ncols_global
-    ops, comm = CudaOps(blk.nloc, stream), (comm_class or NcclComm)(stream)
+    ops, comm = CudaOps(blk.nloc, stream), peer_comm_or_base((comm_class or NcclComm)(stream), stream)
     csr = ops.local_csr(blk)
     # b = A * 1 on this rank's rows (a window of ones times the local rows),
     # outside the clock as in the reference (solver.py:355-358)
@@ -959,6 +1199,7 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
     stream.sync()
     t2 = time.perf_counter()
     res = (dist_cg if method == "cg" else dist_gmres)(A, bvec, params)
+    _finish_comm(comm, res)
     stream.sync()
     t3 = time.perf_counter()
     res["config"] = cfg.token()
@@ -967,6 +1208,17 @@ def distributed_stencil_solve(method: str, dims, offsets, weights, params, model
         timings.update({"predict_s": t1 - t0, "convert_s": t2 - t1, "solve_s": t3 - t2,
                         "total_s": t3 - t0})
     return res, blk
+
+
+def _finish_comm(comm, res: dict):
+    """Report which collectives ran; a PeerComm surfaces a timed-out peer
+    wait and unmaps the peers' buffers (collective)."""
+    res["peer_collectives"] = isinstance(comm, PeerComm)
+    if isinstance(comm, PeerComm):
+        try:
+            comm.check()
+        finally:
+            comm.close()
 
 
 def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=None,
@@ -982,7 +1234,7 @@ def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=N
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     blk = local_block(row_ptr, col_idx, values, r0, r1, n)
     stream = device.thread_stream(+1)
-    ops, comm = CudaOps(blk.nloc, stream), NcclComm(stream)
+    ops, comm = CudaOps(blk.nloc, stream), peer_comm_or_base(NcclComm(stream), stream)
     cfg = initial_config or SpmvConfig(FormatTag.CSR, Library.LIB_B)
     if models is not None:
         from .inference import cascade_predict
@@ -991,6 +1243,7 @@ def distributed_solve(method: str, row_ptr, col_idx, values, b, params, models=N
     A = DistOperator(blk, bounds, comm, ops, cfg)
     b_local = np.asarray(b[r0:r1], dtype=np.float64)
     res = (dist_cg if method == "cg" else dist_gmres)(A, b_local, params)
+    _finish_comm(comm, res)
     res["config"] = cfg.token()
     res["interior_rows"] = A.split
     res["x"] = ops.fetch(res["x"])
@@ -1015,7 +1268,7 @@ def distributed_solve_slab(method: str, r0: int, r1: int, n: int, row_ptr, col_i
     stream = device.thread_stream(0)
     t0 = time.perf_counter()
     blk = slab_block(r0, r1, n, row_ptr, col_idx, values, stream)
-    ops, comm = CudaOps(blk.nloc, stream), (comm_class or NcclComm)(stream)
+    ops, comm = CudaOps(blk.nloc, stream), peer_comm_or_base((comm_class or NcclComm)(stream), stream)
     rows = comm.allgather_obj((int(r0), int(r1)))
     bounds = np.asarray([rows[0][0]] + [r[1] for r in rows], dtype=np.int64)
     if bounds[0] != 0 or bounds[-1] != n or any(rows[k][1] != rows[k + 1][0] for k in range(world - 1)):
@@ -1034,6 +1287,7 @@ def distributed_solve_slab(method: str, r0: int, r1: int, n: int, row_ptr, col_i
     t3 = time.perf_counter()
     res = (dist_cg if method == "cg" else dist_gmres)(A, np.ascontiguousarray(b_local, dtype=np.float64),
                                                        params)
+    _finish_comm(comm, res)
     res["x"] = ops.fetch(res["x"])
     t4 = time.perf_counter()
     res["config"] = cfg.token()

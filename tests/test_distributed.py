@@ -170,6 +170,38 @@ class GlooComm:
             v[:] = t.numpy()
 
 
+class NumpyPeerComm(GlooComm):
+    """Test double of PeerComm's halo push: the x/p pass publishes the rows
+    each neighbour needs (addresses = fake per-rank window bases + the same
+    offset arithmetic DistOperator.setup_push uses), and they land in the
+    window only at wait_halo — after the interior rows ran, as a late
+    NVLink push would — so a misplaced segment or a missing wait changes
+    the solve."""
+
+    def alloc(self, n):
+        return np.zeros(n)
+
+    def share_buffer(self, buf):
+        self._win, self._pending = buf, []
+        return [q << 40 for q in range(self.world)]
+
+    def xp_push(self, n, sc, ialpha, inew, iold, r, p, x, segs):
+        x += sc[ialpha] * p
+        p[:] = r + (sc[inew] / sc[iold]) * p
+        msgs = [(peer, dst, p[lo:lo + cnt].copy()) for lo, cnt, dst, peer in segs]
+        for got in self.allgather_obj(msgs):
+            self._pending += [(dst, d) for peer, dst, d in got if peer == self.rank]
+
+    def wait_halo(self, peers):
+        for dst, d in self._pending:
+            off = (dst - (self.rank << 40)) // 8
+            self._win[off:off + d.size] = d
+        self._pending = []
+
+    def check(self):
+        pass
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -187,7 +219,7 @@ def _worker(rank, world, port, case, q):
         bounds = partition_rows(ptr, world)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         blk = local_block(ptr, cols, vals, r0, r1, n)
-        ops, comm = NumpyOps(blk.nloc), GlooComm()
+        ops, comm = NumpyOps(blk.nloc), (NumpyPeerComm() if case.get("peer") else GlooComm())
         A = DistOperator(blk, bounds, comm, ops, SpmvConfig.from_token(case["cfg"]))
         csr = O.OCsr(n, n, ptr, cols, vals)
         b = O.spmv_sequential(csr, np.ones(n))
@@ -208,7 +240,7 @@ def _worker(rank, world, port, case, q):
         fv = features_from_aggregates(n, n, int(ptr[-1]), agg).to_array().tolist()
         q.put((rank, r0, r1, res["iterations"], res["converged"], res["final"], res["x"], fv,
                HaloPlan.build(bounds, comm.allgather_obj((blk.cmin, blk.cmax)), rank), A.split,
-               res.get("allreduces"), res.get("arnoldi_steps")))
+               res.get("allreduces"), res.get("arnoldi_steps"), res.get("halo_push")))
     finally:
         dist.destroy_process_group()
 
@@ -219,6 +251,11 @@ CASES = {
                             "restart": 40},
     "cg-empty-rank-world4": {"gen": lambda: G.poisson2d(2), "method": "cg", "cfg": "CSR/LibB",
                              "world": 6},
+    "cg-dia-peer-push": {"gen": lambda: G.poisson2d(24), "method": "cg", "cfg": "DIA/LibA", "peer": True},
+    "cg-csr-peer-push-world3": {"gen": lambda: G.poisson2d(30), "method": "cg", "cfg": "CSR/LibB", "world": 3,
+                                "peer": True},
+    "cg-laplace27-peer-push-world4": {"gen": lambda: G.laplace27(12), "method": "cg", "cfg": "DIA/LibA",
+                                      "world": 4, "peer": True},
     "gmres-empty-rank-world5": {"gen": lambda: G.convdiff9(2), "method": "gmres", "cfg": "CSR/LibB",
                                 "world": 5},
     "gmres-convdiff-csr": {"gen": lambda: G.convdiff9(20), "method": "gmres", "cfg": "CSR/LibB"},
@@ -256,6 +293,8 @@ def test_row_partitioned_solve_world2(name):
     if case["method"] == "gmres":                       # CGS2: two all-reduces per Arnoldi step
         for o in outs:
             assert o[10] <= 2 * o[11] + 2 + 3 * 4, (o[10], o[11])
+    if case.get("peer"):                                # the halo travelled by push, not exchange
+        assert all(o[12] for o in outs)
     for o in outs:
         assert o[3] == outs[0][3]                       # ranks agree
         assert o[4] and o[5] <= 1e-8

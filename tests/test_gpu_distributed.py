@@ -107,12 +107,15 @@ def test_distributed_stencil_solve_world1(nccl_world1, method, dims):
     assert t["total_s"] > 0
 
 
-def _world2_worker(rank, port, method, dims, q):
+def _world2_worker(rank, port, method, dims, q, cfg=None, p2p="1"):
     """One of two ranks sharing the single test GPU: CUDA kernels, device
-    halo windows and device scalars, collectives staged through gloo."""
+    halo windows and device scalars; collectives staged through gloo
+    (HostStagedComm) or, with p2p="1", the peer-memory layer on top of it
+    (PeerComm over CUDA IPC between the two processes: mailbox all-reduces,
+    halo pushed by the x/p pass)."""
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPMVTUNE_P2P=p2p)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=2)
     try:
@@ -120,10 +123,16 @@ def _world2_worker(rank, port, method, dims, q):
         offs, w = _stencil(dims)
         params = P.GmresParams(restart_m=30, tol=1e-8, max_iters=3000)
         models = P.CascadeModelSet.load_dir(os.path.join(os.path.dirname(__file__), "golden", "models"))
-        res, blk = distributed_stencil_solve(method, dims, offs, w, params, models=models,
-                                             comm_class=HostStagedComm)
+        if cfg is None:
+            res, blk = distributed_stencil_solve(method, dims, offs, w, params, models=models,
+                                                 comm_class=HostStagedComm)
+        else:
+            res, blk = distributed_stencil_solve(method, dims, offs, w, params,
+                                                 initial_config=P.SpmvConfig.from_token(cfg),
+                                                 comm_class=HostStagedComm)
         q.put((rank, blk.r0, blk.r1, res["iterations"], res["converged"], res["final"],
-               res["x"].to_numpy(), res["config"], blk.cmin, blk.cmax, res["interior_rows"]))
+               res["x"].to_numpy(), res["config"], blk.cmin, blk.cmax, res["interior_rows"],
+               res.get("peer_collectives"), res.get("halo_push")))
     except Exception as exc:          # surface worker failures in the parent
         import traceback
         q.put((rank, "error", repr(exc) + traceback.format_exc()[-1500:]))
@@ -144,8 +153,10 @@ def _stencil(dims):
     return offs, [8.5 if o == (0, 0) else -1.0 - 0.25 * (o[1] + o[0]) for o in offs]
 
 
-@pytest.mark.parametrize("method,dims", [("cg", (14, 12, 10)), ("gmres", (44, 40))])
-def test_cuda_path_world2_on_one_gpu(method, dims):
+@pytest.mark.parametrize("method,dims,cfg,p2p", [("cg", (14, 12, 10), None, "1"), ("gmres", (44, 40), None, "1"),
+                                                 ("cg", (14, 12, 10), "DIA/LibA", "1"),
+                                                 ("cg", (14, 12, 10), "DIA/LibA", "0")])
+def test_cuda_path_world2_on_one_gpu(method, dims, cfg, p2p):
     """World size 2 of the CUDA row-partitioned path (two processes on the
     one GPU, gloo-staged collectives): the halo exchange really moves planes
     between ranks, interior rows are multiplied while it is in flight;
@@ -157,7 +168,7 @@ def test_cuda_path_world2_on_one_gpu(method, dims):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_world2_worker, args=(r, port, method, dims, q)) for r in range(2)]
+    procs = [ctx.Process(target=_world2_worker, args=(r, port, method, dims, q, cfg, p2p)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
@@ -172,7 +183,12 @@ def test_cuda_path_world2_on_one_gpu(method, dims):
     mv = lambda v: O.spmv("CSR/LibB", csr, v)      # noqa: E731
     ref = O.cg(mv, b, tol=1e-8, max_iters=3000) if method == "cg" else \
         O.gmres(mv, b, restart=30, tol=1e-8, max_iters=3000)
-    (_, a0, a1, it0, c0, f0, x0, cfg0, _, cmax0, sp0), (_, b0, b1, it1, c1, f1, x1, cfg1, cmin1, _, sp1) = out
+    (_, a0, a1, it0, c0, f0, x0, cfg0, _, cmax0, sp0, pc0, hp0), \
+        (_, b0, b1, it1, c1, f1, x1, cfg1, cmin1, _, sp1, pc1, hp1) = out
+    # the peer-memory layer ran (CUDA IPC between the two processes) unless disabled
+    assert pc0 == pc1 == (p2p == "1")
+    if method == "cg":
+        assert hp0 == hp1 == (p2p == "1")      # the halo travelled by push in the x/p pass
     assert a0 == 0 and a1 == b0 and b1 == n and cmax0 >= a1 and cmin1 < b0   # real halos both ways
     # the interior rows' SpMV ran before the halo landed (HostStagedComm
     # writes it at exchange_finish), the boundary rows after
@@ -181,6 +197,9 @@ def test_cuda_path_world2_on_one_gpu(method, dims):
     assert abs(it0 - ref["iterations"]) <= 1
     x = np.concatenate([x0, x1])
     assert np.linalg.norm(x - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+    if cfg is not None:
+        assert cfg0 == cfg1 == cfg
+        return
     fv = P.extract_features(P.CsrMatrix(n, n, ptr, cols, vals))
     assert cfg0 == cfg1 == P.cascade_predict(
         P.CascadeModelSet.load_dir(os.path.join(os.path.dirname(__file__), "golden", "models")), fv).token()
