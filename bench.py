@@ -505,8 +505,10 @@ def b200_arm(args):
                 "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload5(), "parallelism": f"row-partitioned x{ws}",
-                           "comm": "gloo, host-staged (path validation, not a performance number)"
-                           if host_staged else "nccl",
+                           "comm": ("gloo, host-staged (path validation, not a performance number)"
+                                    if host_staged else "nccl") + (
+                               "; per-iteration all-reduces and halo by peer-memory kernels (PeerComm)"
+                               if ws > 1 and os.environ.get("SPMVTUNE_P2P", "1") != "0" else ""),
                            "l2": "inputs larger than L2 (47 GB DIA + 71.5 GB CSR per GPU at N=1, 126 MB L2)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk, "detail": detail}
