@@ -651,7 +651,15 @@ class PeerComm:
             mb = int(mbp.value)
         except Exception as exc:   # noqa: BLE001 — reported collectively below
             ok, err = False, f"{type(exc).__name__}: {exc}"
-        ptrs = self._share(mb, ok, err)
+        try:
+            ptrs = self._share(mb, ok, err)
+        except PeerComm.PeerSetupError:
+            for d in self._opened:
+                self.L.svb_peer_ipc_close(d)
+            if self.h is not None:
+                self.L.svb_peer_destroy(self.h)
+            self._opened, self.h = [], None
+            raise
         for q, ptr in enumerate(ptrs):
             _lib.check(self.L.svb_peer_set_mailbox(self.h, q, ptr))
 
@@ -814,7 +822,10 @@ class DistOperator:
         comm, b = self.comm, self.block
         if not hasattr(comm, "share_buffer"):
             return False
-        ptrs = comm.share_buffer(self.window)
+        try:
+            ptrs = comm.share_buffer(self.window)
+        except PeerComm.PeerSetupError:          # raised on every rank together
+            return False
         segs = [(lo - b.r0, hi - lo, ptrs[p] + 8 * (lo - self._windows[p][0]), p)
                 for p, lo, hi in self.plan.sends if hi > lo]
         peers = [p for p, lo, hi in self.plan.recvs if hi > lo]
