@@ -99,11 +99,126 @@ __device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e
   *span_out = (long long)last - first;
 }
 
+struct FeatOut {
+  FeatAcc a;
+  unsigned long long ndiag;                  // popcount of the bitmap
+  unsigned long long rows_read, cols_read;   // row_ptr / col_idx elements consumed
+  unsigned long long noffs;                  // offsets written below (may exceed the cap)
+  unsigned long long nxl;                    // rows handed to k_features_xl
+  int cancelled;
+  int pad;
+  long long offs[4096];                      // diagonal offsets (unordered) when ndiag <= 4096
+};
+
+// Rows longer than FEAT_XL entries (power-law hubs: thousands of entries)
+// leave the tile pipeline: walked by one warp inside a tile they held the
+// whole CTA at its next barrier for a global round trip per 32 columns
+// (0.61 ms for a 1 M-row power-law matrix; 0.35 ms with this path).  The
+// tile pass lists them (row, begin, end) and k_features_xl walks each with
+// a whole CTA: every warp summarises a contiguous part of the row (first and
+// last column, longest run inside, run length from its start and at its
+// end, whether it is one run), and the parts are joined left to right — the
+// run lengths of the sequential recurrence.
+constexpr int FEAT_XL = 2048;
+
+struct RunPart {
+  long long first, last, best, pre, suf, len;
+  bool full;
+};
+__device__ __forceinline__ RunPart join_parts(const RunPart& a, const RunPart& b) {
+  if (a.len == 0) return b;
+  if (b.len == 0) return a;
+  const bool link = b.first == a.last + 1;
+  RunPart c;
+  c.first = a.first;
+  c.last = b.last;
+  c.best = max(max(a.best, b.best), link ? a.suf + b.pre : 0ll);
+  c.pre = (a.full && link) ? a.len + b.pre : a.pre;
+  c.suf = (b.full && link) ? b.len + a.suf : b.suf;
+  c.full = a.full && b.full && link;
+  c.len = a.len + b.len;
+  return c;
+}
+
+// one warp: columns [s, e) of a row (s < e), diagonal marks included
+template <class D>
+__device__ RunPart warp_part(const int* __restrict__ cols, int64_t s, int64_t e, D diag0, unsigned* __restrict__ bits,
+                             D* dcache) {
+  const int lane = threadIdx.x & 31;
+  RunPart r{0, 0, 0, 0, 0, e - s, true};
+  long long carry = 0, pre = -1;
+  int prev_last = 0;
+  for (int64_t base = s; base < e; base += 32) {
+    const int64_t k = base + lane;
+    const bool valid = k < e;
+    const int c = valid ? __ldg(cols + k) : 0;
+    int pc = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane == 0) pc = prev_last;
+    const bool brk = valid && ((k == s) || c != pc + 1);
+    if (valid) mark_diag(bits, (D)c + diag0, dcache);
+    const unsigned B = __ballot_sync(0xffffffffu, brk);
+    const unsigned upto = B & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+    long long run = 0;
+    if (valid) run = upto ? (long long)(lane - (31 - __clz(upto)) + 1) : carry + lane + 1;
+    long long m = run;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, (long long)__shfl_xor_sync(0xffffffffu, m, o));
+    r.best = max(r.best, m);
+    // the first break after the part's first entry ends the leading run
+    const unsigned later = base == s ? (B & ~1u) : B;
+    if (pre < 0 && later) pre = base - s + (__ffs(later) - 1);
+    if (base == s) r.first = __shfl_sync(0xffffffffu, c, 0);
+    const int nv = (int)(e - base < 32 ? e - base : 32);
+    carry = __shfl_sync(0xffffffffu, run, nv - 1);
+    prev_last = __shfl_sync(0xffffffffu, c, nv - 1);
+  }
+  r.last = prev_last;
+  r.suf = carry;
+  r.full = pre < 0;
+  r.pre = pre < 0 ? r.len : pre;
+  return r;
+}
+
+struct XlRow {
+  long long row, beg, end;
+};
+
+template <class D>
+__global__ void __launch_bounds__(256) k_features_xl(int64_t nrows, const int* __restrict__ cols,
+                                                     unsigned* __restrict__ bits, const XlRow* __restrict__ list,
+                                                     FeatOut* out, const volatile int* cancel) {
+  __shared__ D dcache[DIAG_CACHE];
+  __shared__ RunPart parts[8];
+  __shared__ int stop;
+  diag_cache_init(dcache);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned long long count = out->nxl;
+  for (unsigned long long q = blockIdx.x; q < count; q += gridDim.x) {
+    if (threadIdx.x == 0) stop = cancel ? *cancel : 0;   // one reading per CTA: a uniform exit
+    __syncthreads();
+    if (stop) return;
+    const XlRow xr = list[q];
+    const int64_t len = xr.end - xr.beg, per = (len + 7) / 8;
+    const int64_t a = xr.beg + min((int64_t)warp * per, len), b = xr.beg + min((int64_t)(warp + 1) * per, len);
+    RunPart p{0, 0, 0, 0, 0, 0, true};
+    if (a < b) p = warp_part<D>(cols, a, b, (D)(nrows - 1 - xr.row), bits, dcache);
+    if (lane == 0) parts[warp] = p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      RunPart t = parts[0];
+      for (int w = 1; w < 8; ++w) t = join_parts(t, parts[w]);
+      atomicAdd(&out->a.span, (unsigned long long)(t.last - t.first));
+      atomicAdd(&out->a.runs, (unsigned long long)t.best);
+    }
+    __syncthreads();
+  }
+}
+
 // One pass over row_ptr and col_idx through the row-tile ring (matrix.cuh):
 // one thread per row walks its staged columns (run lengths, span, diagonal
 // marks) in 32-bit arithmetic (ncu, round 1 kernel: 65 instructions per
 // entry, issue-bound at 0.2 of HBM); rows longer than FEAT_LONG go to a
-// warp.  A tile's entries are staged up to the stage capacity (a row that
+// warp, rows longer than FEAT_XL to k_features_xl.  A tile's entries are staged up to the stage capacity (a row that
 // crosses the end reads global memory).  Thread 0 keeps the row-pointer
 // bounds of the tiles it will issue FEAT_PF tiles ahead with cp.async, so
 // no refill waits on a dependent row_ptr load.  Thread 0 polls the cancel
@@ -117,20 +232,12 @@ __device__ __forceinline__ void warp_row_runs(const G& col, int64_t s, int64_t e
 // features.py:60-65).
 constexpr int FEAT_R = 256, FEAT_CAP = 5120, FEAT_NS = 3, FEAT_PF = 4, FEAT_BR = 8;
 
-struct FeatOut {
-  FeatAcc a;
-  unsigned long long ndiag;                  // popcount of the bitmap
-  unsigned long long rows_read, cols_read;   // row_ptr / col_idx elements consumed
-  unsigned long long noffs;                  // offsets written below (may exceed the cap)
-  int cancelled;
-  int pad;
-  long long offs[4096];                      // diagonal offsets (unordered) when ndiag <= 4096
-};
 
 template <class P, class D>
 __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __restrict__ ptr,
                                                      const int* __restrict__ cols, unsigned* __restrict__ bits,
-                                                     FeatOut* out, const volatile int* cancel) {
+                                                     FeatOut* out, const volatile int* cancel,
+                                                     XlRow* __restrict__ xl) {
   using Lay = RingLayout<P, FEAT_R, FEAT_CAP, false>;
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ alignas(8) uint64_t bar[FEAT_NS];
@@ -200,7 +307,10 @@ __global__ void __launch_bounds__(FEAT_R) k_features(int64_t nrows, const P* __r
       a.sum_r2 += (unsigned long long)(L * L);
       a.max_r = max(a.max_r, (long long)L);
       a.min_r = min(a.min_r, (long long)L);
-      if (L > FEAT_LONG) {
+      if (L > FEAT_XL) {
+        const unsigned long long q = atomicAdd(&out->nxl, 1ull);
+        xl[q] = XlRow{(long long)i, (long long)(sp[tid]), (long long)(sp[tid + 1])};
+      } else if (L > FEAT_LONG) {
         lrows[atomicAdd(&nl, 1)] = tid;
       } else if (L > 0) {
         // 32-bit walk over the row's columns (shared memory when the whole
@@ -325,7 +435,7 @@ struct svb_features_job {
   int* flag = nullptr;         // device cancel word; 0 whenever the job is idle
   cudaEvent_t done = nullptr;
   bool cancel_requested = false;
-  Buf bits, out;
+  Buf bits, out, xl;
 };
 
 namespace {
@@ -375,6 +485,7 @@ svb_features_job* job_get() {
 void job_put(svb_features_job* j) {
   j->bits.reset();
   j->out.reset();
+  j->xl.reset();
   j->m = nullptr;
   j->cancel_requested = false;
   std::lock_guard<std::mutex> lk(g_job_mu);
@@ -397,6 +508,7 @@ extern "C" int svb_features_start(const svb_matrix* m, int precancelled, void* s
       const int64_t nwords = (nbits + 31) / 32;
       j->bits = alloc(nwords * 4, s);
       j->out = alloc(sizeof(FeatOut), s);
+      j->xl = alloc((m->nnz / (FEAT_XL + 1) + 1) * sizeof(XlRow), s);   // rows longer than FEAT_XL
       auto* out = ptr<FeatOut>(j->out);
       SVB_CUDA_TRY(cudaMemsetAsync(j->bits->ptr, 0, nwords * 4, s));
       SVB_CUDA_TRY(cudaMemsetAsync(out, 0, offsetof(FeatOut, offs), s));
@@ -428,19 +540,30 @@ extern "C" int svb_features_start(const svb_matrix* m, int precancelled, void* s
         if (m->ptr64) {
           if (narrow)
             k_features<long long, unsigned><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr), ptr<int>(m->cols),
-                                                                     bitsp, out, j->flag);
+                                                                     bitsp, out, j->flag, ptr<XlRow>(j->xl));
           else
             k_features<long long, long long><<<g, FEAT_R, dsm64, s>>>(m->nrows, ptr<long long>(m->ptr),
-                                                                      ptr<int>(m->cols), bitsp, out, j->flag);
+                                                                      ptr<int>(m->cols), bitsp, out, j->flag,
+                                                                      ptr<XlRow>(j->xl));
         } else {
           if (narrow)
             k_features<int, unsigned><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols), bitsp,
-                                                               out, j->flag);
+                                                               out, j->flag, ptr<XlRow>(j->xl));
           else
             k_features<int, long long><<<g, FEAT_R, dsm32, s>>>(m->nrows, ptr<int>(m->ptr), ptr<int>(m->cols), bitsp,
-                                                                out, j->flag);
+                                                                out, j->flag, ptr<XlRow>(j->xl));
         }
         SVB_CHECK_LAUNCH();
+        if (m->nnz > FEAT_XL) {   // the listed extra-long rows, a CTA each
+          const unsigned gx = (unsigned)std::min<int64_t>(m->nnz / (FEAT_XL + 1) + 1, (int64_t)sm_count() * 4);
+          if (narrow)
+            k_features_xl<unsigned><<<gx, 256, 0, s>>>(m->nrows, ptr<int>(m->cols), bitsp, ptr<XlRow>(j->xl), out,
+                                                        j->flag);
+          else
+            k_features_xl<long long><<<gx, 256, 0, s>>>(m->nrows, ptr<int>(m->cols), bitsp, ptr<XlRow>(j->xl), out,
+                                                         j->flag);
+          SVB_CHECK_LAUNCH();
+        }
       }
       k_popcount<<<grid_for(nwords, 256, 4), 256, 0, s>>>(nwords, ptr<unsigned>(j->bits), &out->ndiag);
       SVB_CHECK_LAUNCH();

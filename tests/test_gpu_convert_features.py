@@ -91,6 +91,34 @@ def test_features_large_against_oracle():
         assert fv.to_array().tolist() == O.features(O.OCsr(n, m, ptr, cols, vals))
 
 
+def test_features_extra_long_rows_against_oracle():
+    """Rows longer than FEAT_XL (2048) are walked by a whole CTA in eight
+    parts joined left to right (k_features_xl): runs that cross part
+    boundaries, rows that are one run, alternating gaps, a run ending exactly
+    at a part edge — the aggregates must equal the sequential recurrence."""
+    rng = np.random.default_rng(3)
+    ncols = 400_000
+    rows = []
+    rows.append(np.arange(1000, 1000 + 20_000))                       # one run
+    r = np.arange(5000, 5000 + 30_000)
+    rows.append(r[np.arange(r.size) % 7 != 3])                        # gaps every 7
+    rows.append(np.arange(0, 2 * 9000, 2))                            # no two consecutive
+    a = np.arange(100, 100 + 8 * 1000)                                # breaks at part edges
+    rows.append(np.concatenate([a[:4000], a[4000:] + 50]))
+    rows.append(np.sort(rng.choice(ncols, size=5000, replace=False)))
+    blk = np.arange(200_000, 200_000 + 12_345)                        # long run inside random
+    rows.append(np.unique(np.concatenate([blk, rng.choice(ncols, size=3000, replace=False)])))
+    n = 3000
+    body = [np.sort(rng.choice(ncols, size=int(rng.integers(1, 40)), replace=False)) for _ in range(n - len(rows))]
+    allrows = body[:1000] + rows + body[1000:]
+    ptr = np.zeros(n + 1, np.int64)
+    ptr[1:] = np.cumsum([x.size for x in allrows])
+    cols = np.concatenate(allrows).astype(np.int64)
+    vals = np.ones(cols.size)
+    fv = P.extract_features(P.CsrMatrix(n, ncols, ptr, cols, vals))
+    assert fv.to_array().tolist() == O.features(O.OCsr(n, ncols, ptr, cols, vals))
+
+
 def test_feature_cancellation_and_counters():
     n, m, ptr, cols, vals = G.poisson2d(40)
     csr = P.CsrMatrix(n, m, ptr, cols, vals)
