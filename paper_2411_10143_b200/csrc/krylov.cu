@@ -39,7 +39,7 @@ struct svb_krylov {
   // TMA-streamed MGS (mgs_tma.cuh, the default when the slice fits): launch
   // plan, tagged exchange slots and the per-launch epoch of the tags
   bool tma = false;
-  int tma_chunks = 0, tma_stages = 0;
+  int tma_chunks = 0, tma_stages = 0, tma_nres = 0;
   unsigned long long epoch = 0;
   svb::Buf gslot;
   // recorded right after every status-producing kernel: the host waits on
@@ -1259,17 +1259,18 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
       const char* mode = std::getenv("SPMVTUNE_MGS");
       const bool allowed = !(mode && std::strcmp(mode, "stream") == 0);
       // TMA-streamed MGS: w in registers + smem, V_{i-1} in TMEM, the basis
-      // rows streamed once through a bulk-copy ring.  Its own plan() bounds
-      // it (a slice of at most mgs::MAX_SLICE = 32768 doubles: n <= 4.85 M
-      // on 148 SMs), independent of the older SM-resident kernel's limit
+      // rows streamed once through a bulk-copy ring; slices above the
+      // on-chip capacity (mgs::MAX_SLICE = 32768 doubles: n > 4.85 M on 148
+      // SMs) run partially resident up to n = 19.4 M (mgs::plan)
       const bool tma_ok = !(mode && (std::strcmp(mode, "resident") == 0 || std::strcmp(mode, "tmem") == 0)) &&
                           m + 2 < 255;
-      if (allowed && coop && m >= 1 && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages) &&
+      if (allowed && coop && m >= 1 && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages, &k->tma_nres) &&
           mgs::SMEM <= (size_t)optin) {
-        SVB_CUDA_TRY(cudaFuncSetAttribute(mgs::k_mgs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)mgs::SMEM));
+        const void* kern = k->tma_nres < k->tma_chunks ? (const void*)mgs::k_mgs_tma<true>
+                                                       : (const void*)mgs::k_mgs_tma<false>;
+        SVB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mgs::SMEM));
         int per = 0;
-        SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mgs::k_mgs_tma, mgs::NT, mgs::SMEM));
+        SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, mgs::NT, mgs::SMEM));
         if (per >= 1) {
           k->tma = true;
           const size_t gb = 2 * (size_t)mgs::SLOT_STRIDE * G * sizeof(unsigned long long);
@@ -1414,10 +1415,12 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
       A.epoch = ++k->epoch;
       A.chunk_count = k->tma_chunks;
       A.nsb = k->tma_stages;
+      A.nres = k->tma_nres;
       A.trace = nullptr;
       void* args[] = {&A};
-      SVB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)mgs::k_mgs_tma, dim3(sm_count()), dim3(mgs::NT), args,
-                                               mgs::SMEM, s));
+      const void* kern = k->tma_nres < k->tma_chunks ? (const void*)mgs::k_mgs_tma<true>
+                                                     : (const void*)mgs::k_mgs_tma<false>;
+      SVB_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(sm_count()), dim3(mgs::NT), args, mgs::SMEM, s));
       note_launches(1);
       k->normalized = j;
       mark(k, s);

@@ -24,6 +24,15 @@
 //
 // HBM traffic per step: w once, each V_i once, V[j+1] written once:
 // 8n(j+3) bytes, the algorithmic minimum.
+//
+// Slices longer than the on-chip capacity (MAXCH chunks: n > 148 x 32768 =
+// 4.85 M rows) run partially resident: chunks [0, nres) as above, chunks
+// [nres, nch) ("overflow") keep w in global memory — in the V[j+1] row it
+// will be normalised into, each consumer thread loading and storing only its
+// own elements (program order makes its stores visible to its next loads) —
+// and re-stream V_{i-1} next to V_i instead of parking it in TMEM: 32 bytes
+// per overflow element per pass instead of 8, against the 32n of the
+// streaming fallback for every element.
 #pragma once
 
 #include <cstdint>
@@ -47,6 +56,7 @@ constexpr int TCOLS = 512;
 constexpr int SLOT_STRIDE = 32;         // words between exchange slots (256 B)
 constexpr int HDR = 1024;               // barriers + scratch + TMEM base, ahead of w / ring
 constexpr size_t SMEM = 232448;         // the whole opt-in shared memory: one CTA per SM
+constexpr int MAXCH_OV = 64;            // chunks per slice with overflow (n <= 148 x 131072 = 19.4 M)
 
 struct Args {
   double* V;            // basis rows, row stride ld
@@ -62,6 +72,7 @@ struct Args {
   unsigned long long epoch;   // distinct per launch
   int chunk_count;             // chunks in a full slice (plan())
   int nsb;                     // ring stages (plan())
+  int nres;                    // chunks of a slice kept on chip (plan(); < chunk_count: overflow mode)
   unsigned long long* trace;  // optional: [grid][npass][4] globaltimer stamps (profiling)
 };
 
@@ -260,6 +271,9 @@ __device__ __forceinline__ void sts2(double* p, double x, double y) {
   *reinterpret_cast<double2*>(p) = make_double2(x, y);
 }
 
+// OV: the partially resident (overflow) mode; OV = false compiles the
+// fully resident kernel alone (no extra register pressure on its path)
+template <bool OV>
 __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // NSB_MAX
@@ -274,7 +288,9 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   const int len = hi > lo ? (int)(hi - lo) : 0;
   const int nch = (len + E - 1) / E;
   const int nsb = A.nsb;
-  double* ring = wsm + (size_t)(A.chunk_count > R ? A.chunk_count - R : 0) * E;   // nsb x E
+  const int nres = OV ? A.nres : A.chunk_count;
+  const int nrc = OV ? (nch < nres ? nch : nres) : nch;   // this slice's resident chunks
+  double* ring = wsm + (size_t)(nres > R ? nres - R : 0) * E;   // nsb x E
   const int j = A.j;
   const int npass = j + 2;   // pass 0 (w, V_0), passes 1..j (V_i), final
 
@@ -318,11 +334,16 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
         }
       };
       for (int q = 0; q < nch; ++q) {
-        put(row(j + 1), q);
+        if (!OV || q < nres) put(row(j + 1), q);   // overflow w is read by the consumers themselves
         put(row(0), q);
       }
       for (int p = 1; p <= j; ++p)
-        for (int q = 0; q < nch; ++q) put(row(p), q);
+        for (int q = 0; q < nch; ++q) {
+          if (OV && q >= nres) put(row(p - 1), q);   // V_{p-1} of overflow chunks: not in TMEM
+          put(row(p), q);
+        }
+      if (OV)
+        for (int q = nres; q < nch; ++q) put(row(j), q);   // final pass, overflow chunks
     }
     return;
   }
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
     }                                                                                           \
     _Pragma("unroll") for (int k = 0; k < GQ; ++k) {                                            \
       const int q = GQ * (g) + k;                                                               \
-      if (q < nch) {                                                                            \
+      if (q < nrc) {                                                                            \
         const int lim = len - q * E;                                                            \
         const bool fullc = lim >= E;                                                            \
         if (KIND == 0) {                                                                        \
@@ -418,6 +439,71 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
     if (KIND < 2) t_st32(ta, pv);                                                               \
   }
 
+  // overflow chunks [nres, nch): w in the V[j+1] row (this thread's own
+  // pairs, loaded one chunk ahead), V_{p-1} streamed next to V_p
+  double* wov = A.V + (int64_t)(j + 1) * A.ld + lo + e0;
+  auto ov_load = [&](int q, double (&w)[U]) {
+    const int lim = len - q * E;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const double* a = wov + (int64_t)q * E + 2 * CT * i;
+      if (lim >= E || ok1(i, lim)) {
+        const double2 t = __ldcg(reinterpret_cast<const double2*>(a));
+        w[2 * i] = t.x;
+        w[2 * i + 1] = t.y;
+      } else {
+        w[2 * i] = ok0(i, lim) ? __ldcg(a) : 0.0;
+        w[2 * i + 1] = 0.0;
+      }
+    }
+  };
+  auto ov_store = [&](int q, const double (&w)[U]) {
+    const int lim = len - q * E;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      double* a = wov + (int64_t)q * E + 2 * CT * i;
+      if (lim >= E || ok1(i, lim)) __stcg(reinterpret_cast<double2*>(a), make_double2(w[2 * i], w[2 * i + 1]));
+      else if (ok0(i, lim)) __stcg(a, w[2 * i]);
+    }
+  };
+  auto ov_pass = [&](int kind, double& acc) {
+    if (nch <= nrc) return;
+    double cur[U], nxt[U];
+    ov_load(nrc, cur);
+#pragma unroll 1
+    for (int q = nrc; q < nch; ++q) {
+      if (q + 1 < nch) ov_load(q + 1, nxt);
+      const int lim = len - q * E;
+      const bool fullc = lim >= E;
+      if (kind > 0) {   // w -= h_{p-1} V_{p-1}
+        const double* sp = take();
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          Pair t = lds2(sp + 2 * CT * i);
+          cur[2 * i] -= h * (fullc || ok0(i, lim) ? t.x : 0.0);
+          cur[2 * i + 1] -= h * (fullc || ok1(i, lim) ? t.y : 0.0);
+        }
+        give();
+      }
+      if (kind < 2) {   // acc += V_p . w
+        const double* sv = take();
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          Pair t = lds2(sv + 2 * CT * i);
+          acc += (fullc || ok0(i, lim) ? t.x : 0.0) * cur[2 * i];
+          acc += (fullc || ok1(i, lim) ? t.y : 0.0) * cur[2 * i + 1];
+        }
+        give();
+      } else {          // acc += w . w
+#pragma unroll
+        for (int i = 0; i < U; ++i) acc += cur[i] * cur[i];
+      }
+      if (kind > 0) ov_store(q, cur);
+#pragma unroll
+      for (int i = 0; i < U; ++i) cur[i] = nxt[i];
+    }
+  };
+
   auto finish_pass = [&](int p, double acc) {
     t_wait_st();
     // CTA reduction (fixed order) then grid exchange
@@ -462,10 +548,11 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
 #define WS_SM(k, i, wx, wy) sts2(WADDR(k, i), (wx), (wy))
 #define MGS_PASS(KIND)                                                            \
   {                                                                               \
-    _Pragma("unroll") for (int g = 0; g < R / GQ; ++g) if (GQ * g < nch)          \
+    _Pragma("unroll") for (int g = 0; g < R / GQ; ++g) if (GQ * g < nrc)          \
         MGS_GROUP(KIND, g, WL_REG, WS_REG)                                        \
-    _Pragma("unroll 1") for (int g = R / GQ; GQ * g < nch; ++g)                   \
+    _Pragma("unroll 1") for (int g = R / GQ; GQ * g < nrc; ++g)                   \
         MGS_GROUP(KIND, g, WL_SM, WS_SM)                                          \
+    if constexpr (OV) ov_pass(KIND, acc);                                         \
   }
   {  // pass 0: stage w, h_0 = V_0 . w, V_0 -> TMEM
     const int p = 0;
@@ -509,16 +596,25 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   };
 #pragma unroll
   for (int q = 0; q < R; ++q)
-    if (q < nch) {
+    if (q < nrc) {
 #pragma unroll
       for (int i = 0; i < NP; ++i) put_w(q, wr[q][2 * i], wr[q][2 * i + 1], i);
     }
 #pragma unroll 1
-  for (int q = R; q < nch; ++q) {
+  for (int q = R; q < nrc; ++q) {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const Pair t = lds2(wsm + (size_t)(q - R) * E + e0 + 2 * CT * i);
       put_w(q, t.x, t.y, i);
+    }
+  }
+  if constexpr (OV) {
+#pragma unroll 1
+    for (int q = nrc; q < nch; ++q) {   // overflow: w is already in place in the V[j+1] row
+      double w[U];
+      ov_load(q, w);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) put_w(q, w[2 * i], w[2 * i + 1], i);
     }
   }
   if (lead) givens(A, hnext);
@@ -530,17 +626,20 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   }
 }
 
-// host-side launch geometry for a slice of `chunk` elements
-inline bool plan(int64_t chunk, int* chunk_count, int* nsb) {
+// host-side launch geometry for a slice of `chunk` elements; nres < the
+// chunk count selects the partially resident (overflow) mode
+inline bool plan(int64_t chunk, int* chunk_count, int* nsb, int* nres) {
   const int nch = (int)((chunk + E - 1) / E);
-  if (chunk > MAX_SLICE) return false;
-  const int wch = nch > R ? nch - R : 0;
+  if (nch > MAXCH_OV) return false;
+  const int res = nch < MAXCH ? nch : MAXCH;
+  const int wch = res > R ? res - R : 0;
   const int64_t room = (int64_t)SMEM - HDR - (int64_t)wch * E * 8;
   int s = (int)(room / (E * 8));
   if (s > NSB_MAX) s = NSB_MAX;
   if (s < 2) return false;
   *chunk_count = nch;
   *nsb = s;
+  *nres = res;
   return true;
 }
 

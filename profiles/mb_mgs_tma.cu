@@ -53,7 +53,7 @@ int main(int argc, char** argv) {
   CK(cudaMemset(cs, 0, m * 8));
   CK(cudaMemset(sn, 0, m * 8));
   CK(cudaMemset(g, 0, (m + 1) * 8));
-  CK(cudaFuncSetAttribute(k_mgs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  CK(cudaFuncSetAttribute(k_mgs_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
   unsigned long long epoch = 1;
   Args A{};
   A.V = V;
@@ -68,7 +68,7 @@ int main(int argc, char** argv) {
   A.st = st;
   A.bnorm = 1.0;
   A.gslot = gslot;
-  if (!plan(chunk, &A.chunk_count, &A.nsb)) {
+  if (!plan(chunk, &A.chunk_count, &A.nsb, &A.nres)) {
     printf("no plan\n");
     return 1;
   }
@@ -77,7 +77,7 @@ int main(int argc, char** argv) {
     A.j = j;
     A.epoch = epoch++;
     void* args[] = {&A};
-    CK(cudaLaunchCooperativeKernel((const void*)k_mgs_tma, dim3(G), dim3(NT), args, SMEM, 0));
+    CK(cudaLaunchCooperativeKernel((const void*)k_mgs_tma<false>, dim3(G), dim3(NT), args, SMEM, 0));
   };
   // ---- correctness at several j against a CPU MGS
   int bad = 0;

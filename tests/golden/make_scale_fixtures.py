@@ -64,6 +64,8 @@ def matrix(name: str):
         return G.powerlaw_spd(8_000_000, seed=0)
     if name == "config5_120":
         return G.laplace27(120)     # config 5's matrix family at 120^3 (600^3 has 5.8 B nnz)
+    if name == "config2_8M":
+        return G.convdiff9(2830)    # config 2's family above the on-chip Arnoldi capacity (4.85 M rows)
     raise KeyError(name)
 
 
@@ -106,7 +108,30 @@ def cg_oracle(csr, tok, b, tol=1e-8, max_iters=20000) -> dict:
             "seconds": time.perf_counter() - t}
 
 
+def build_gmres_only(name: str) -> dict:
+    """config2_8M: the matrix hash and the reference's GMRES(30) on DIA only
+    (the partially resident Arnoldi kernel's parity target)."""
+    t0 = time.perf_counter()
+    n, m, ptr, cols, vals = matrix(name)
+    doc = {"n": int(n), "nnz": int(cols.size),
+           "csr_sha256": sha(np.asarray(ptr, np.int64), np.asarray(cols, np.int64), np.asarray(vals, np.float64))}
+    csr = S.CsrMatrix(n, m, ptr, cols, vals)
+    params = S.GmresParams(restart_m=30, tol=1e-8, max_iters=1000)
+    dia = S.convert(csr, S.FormatTag.DIA)
+    t = time.perf_counter()
+    rep = S.gmres_solve(dia, None, params,
+                        executor=S.SpmvExecutor(S.SpmvConfig(S.FormatTag.DIA, S.Library.LIB_A), dia))
+    doc["gmres30"] = {"iterations": rep.iterations, "converged": rep.converged,
+                      "final_residual": float(rep.final_residual),
+                      "history_head": [float(v) for v in rep.residual_history[:5]],
+                      "seconds": time.perf_counter() - t, "matvec": "DIA/LibA"}
+    doc["seconds"] = time.perf_counter() - t0
+    return doc
+
+
 def build(name: str, models) -> dict:
+    if name == "config2_8M":
+        return build_gmres_only(name)
     t0 = time.perf_counter()
     n, m, ptr, cols, vals = matrix(name)
     print(f"{name}: n={n} nnz={cols.size} generated in {time.perf_counter() - t0:.1f}s", flush=True)

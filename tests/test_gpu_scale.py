@@ -204,6 +204,31 @@ def test_tma_arnoldi_beyond_the_resident_kernels_limit():
     assert a["launches"] / a["iterations"] < 6 < b["launches"] / b["iterations"], res
 
 
+def test_tma_arnoldi_partially_resident_matches_reference():
+    """n = 2830^2 = 8.0 M rows: each SM's slice (54 K doubles) exceeds the
+    on-chip capacity (32 K), so the TMA kernel runs partially resident (16
+    chunks on chip, the rest with w in the V[j+1] row and V_{i-1} streamed):
+    one launch per Arnoldi step, within 1 iteration of the reference's
+    GMRES(30) (fixture config2_8M, made with the reference's own
+    gmres_solve on DIA) and of the streaming fallback."""
+    f = fixtures()["config2_8M"]
+    res = {}
+    for mode in ("default", "stream"):
+        env = dict(os.environ)
+        env.pop("SPMVTUNE_MGS", None)
+        if mode == "stream":
+            env["SPMVTUNE_MGS"] = "stream"
+        out = subprocess.run([sys.executable, "-c", _MGS_GATE_SCRIPT.format(root=str(ROOT), nx=2830)], env=env,
+                             capture_output=True, text=True, timeout=1200)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
+    a, b = res["default"], res["stream"]
+    assert a["converged"] and b["converged"] and a["final"] <= 1e-8 and b["final"] <= 1e-8
+    assert abs(a["iterations"] - f["gmres30"]["iterations"]) <= 1, (a, f["gmres30"])
+    assert abs(a["iterations"] - b["iterations"]) <= 1
+    assert a["launches"] / a["iterations"] < 6 < b["launches"] / b["iterations"], res
+
+
 def test_config1_cg_matches_oracle_iterations():
     c = fixtures()["config1"]["cg"]
     A = matrix("config1")
