@@ -840,6 +840,9 @@ class DistOperator:
         neighbours' last x/p pass: the interior rows run at once, the stream
         then waits on the device for the neighbours' tags, then the boundary
         rows.  ``src`` must be the window's own slice (CG's p)."""
+        if self.no_halo:                   # nothing to receive: the SpMV reads src itself
+            self.apply_dot(src, dst, sc, slot)
+            return
         ops = self.ops
         _, peers = self.push
         fused = hasattr(ops, "spmv_dot")
@@ -1101,7 +1104,7 @@ def dist_cg(A: DistOperator, b_local, params) -> dict:
     # peer-memory mode (PeerComm): the x/p pass pushes the next direction's
     # halo into the neighbours' windows, the next SpMV waits for it on the
     # device — no exchange call in the loop
-    push = (not A.no_halo) and A.setup_push()
+    push = A.setup_push()                 # collective: every rank takes part
     pushed = False
     while done < params.max_iters:
         if pushed:

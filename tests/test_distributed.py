@@ -256,6 +256,8 @@ CASES = {
                                 "peer": True},
     "cg-laplace27-peer-push-world4": {"gen": lambda: G.laplace27(12), "method": "cg", "cfg": "DIA/LibA",
                                       "world": 4, "peer": True},
+    "cg-peer-push-empty-ranks": {"gen": lambda: G.stencil_csr((7,), [(-1,), (0,), (1,)], [-1.0, 2.5, -1.0]),
+                                 "method": "cg", "cfg": "DIA/LibA", "world": 9, "peer": True},
     "gmres-empty-rank-world5": {"gen": lambda: G.convdiff9(2), "method": "gmres", "cfg": "CSR/LibB",
                                 "world": 5},
     "gmres-convdiff-csr": {"gen": lambda: G.convdiff9(20), "method": "gmres", "cfg": "CSR/LibB"},
