@@ -597,6 +597,7 @@ def e2e_slab(args, blk, r0, r1, params, models, comm_class, ws):
     return {"value": float(tt.item()) / k, "unit": "s", "h2d_bytes_per_step": int(byts[0].item()),
             "d2h_bytes_per_step": int(byts[1].item()), "steps": k, "iterations": res["iterations"],
             "converged": res["converged"], "final_residual": res["final"], "phases_last": phases[-1],
+            "phases": phases,
             "host_slab_prep_s": prep_s,
             "note": "each rank: pinned host slab (row_ptr int64, GLOBAL col_idx int32, values f64, b f64) -> "
                     "distributed_solve_slab (H2D + device validation + features + cascade + conversion + "

@@ -50,6 +50,8 @@ constexpr int NT = CT + 32;             // + one producer warp (the HBM stream)
 constexpr int E = 2048;                 // elements per chunk / ring stage (16 KB)
 constexpr int MAXCH = 16;               // chunks per slice the TMEM layout can hold
 constexpr int R = 6;                    // chunks of w held in registers (U doubles each per thread)
+constexpr int R_OV = 4;                 // ... in the overflow mode (its prefetch registers)
+constexpr int MAXCH_RES_OV = 14;        // chunks kept on chip in the overflow mode (same shared memory)
 constexpr int NSB_MAX = 12;             // ring stages at most
 constexpr int64_t MAX_SLICE = (int64_t)E * MAXCH;   // 32768 doubles = 256 KB of TMEM
 constexpr int TCOLS = 512;
@@ -275,12 +277,13 @@ __device__ __forceinline__ void sts2(double* p, double x, double y) {
 // fully resident kernel alone (no extra register pressure on its path)
 template <bool OV>
 __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
+  constexpr int RR = OV ? R_OV : R;   // register-resident chunks of w
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // NSB_MAX
   uint64_t* empty = full + NSB_MAX;                                     // NSB_MAX
   double* scratch = reinterpret_cast<double*>(empty + NSB_MAX);        // 64 doubles
   uint32_t* tbase = reinterpret_cast<uint32_t*>(scratch + 64);
-  double* wsm = reinterpret_cast<double*>(smem_raw + HDR);              // chunks R.. of w
+  double* wsm = reinterpret_cast<double*>(smem_raw + HDR);              // chunks RR.. of w
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t lo = (int64_t)blockIdx.x * A.chunk;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   const int nsb = A.nsb;
   const int nres = OV ? A.nres : A.chunk_count;
   const int nrc = OV ? (nch < nres ? nch : nres) : nch;   // this slice's resident chunks
-  double* ring = wsm + (size_t)(nres > R ? nres - R : 0) * E;   // nsb x E
+  double* ring = wsm + (size_t)(nres > RR ? nres - RR : 0) * E;   // nsb x E
   const int j = A.j;
   const int npass = j + 2;   // pass 0 (w, V_0), passes 1..j (V_i), final
 
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
   const int qd = warp & 3, cg = warp >> 2;
   const uint32_t tw = *tbase + ((uint32_t)(32 * qd) << 16) + (uint32_t)(256 * cg);
   const int e0 = 2 * threadIdx.x;   // first element of pair 0 within a chunk
-  double wr[R][U];
+  double wr[RR][U];
   int rs = 0;
   uint32_t rph = 0;
   double h = 0.0;
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
     wr[GQ * g + (k)][2 * (i) + 1] = (wy); \
   }
   // shared-memory chunks of w
-#define WADDR(k, i) (wsm + (size_t)(GQ * g + (k) - R) * E + e0 + 2 * CT * (i))
+#define WADDR(k, i) (wsm + (size_t)(GQ * g + (k) - RR) * E + e0 + 2 * CT * (i))
 #define WL_SM(k, i, wx, wy)            \
   {                                    \
     const Pair t_ = lds2(WADDR(k, i)); \
@@ -548,9 +551,9 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
 #define WS_SM(k, i, wx, wy) sts2(WADDR(k, i), (wx), (wy))
 #define MGS_PASS(KIND)                                                            \
   {                                                                               \
-    _Pragma("unroll") for (int g = 0; g < R / GQ; ++g) if (GQ * g < nrc)          \
+    _Pragma("unroll") for (int g = 0; g < RR / GQ; ++g) if (GQ * g < nrc)          \
         MGS_GROUP(KIND, g, WL_REG, WS_REG)                                        \
-    _Pragma("unroll 1") for (int g = R / GQ; GQ * g < nrc; ++g)                   \
+    _Pragma("unroll 1") for (int g = RR / GQ; GQ * g < nrc; ++g)                   \
         MGS_GROUP(KIND, g, WL_SM, WS_SM)                                          \
     if constexpr (OV) ov_pass(KIND, acc);                                         \
   }
@@ -595,16 +598,16 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
     }
   };
 #pragma unroll
-  for (int q = 0; q < R; ++q)
+  for (int q = 0; q < RR; ++q)
     if (q < nrc) {
 #pragma unroll
       for (int i = 0; i < NP; ++i) put_w(q, wr[q][2 * i], wr[q][2 * i + 1], i);
     }
 #pragma unroll 1
-  for (int q = R; q < nrc; ++q) {
+  for (int q = RR; q < nrc; ++q) {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-      const Pair t = lds2(wsm + (size_t)(q - R) * E + e0 + 2 * CT * i);
+      const Pair t = lds2(wsm + (size_t)(q - RR) * E + e0 + 2 * CT * i);
       put_w(q, t.x, t.y, i);
     }
   }
@@ -631,8 +634,10 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_tma(Args A) {
 inline bool plan(int64_t chunk, int* chunk_count, int* nsb, int* nres) {
   const int nch = (int)((chunk + E - 1) / E);
   if (nch > MAXCH_OV) return false;
-  const int res = nch < MAXCH ? nch : MAXCH;
-  const int wch = res > R ? res - R : 0;
+  const bool ov = nch > MAXCH;
+  const int res = ov ? MAXCH_RES_OV : nch;
+  const int rr = ov ? R_OV : R;
+  const int wch = res > rr ? res - rr : 0;
   const int64_t room = (int64_t)SMEM - HDR - (int64_t)wch * E * 8;
   int s = (int)(room / (E * 8));
   if (s > NSB_MAX) s = NSB_MAX;
