@@ -26,6 +26,7 @@
 // so they can be exported with CUDA IPC; in one process they are plain
 // device pointers.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -46,6 +47,7 @@ struct PeerView {
   int rank, world;
   Mailbox* mb[PEER_MAXW];   // every rank's mailbox as addressable from this GPU (own included)
   int* err;                 // mapped host word, raised by a wait that passed its deadline
+  unsigned long long deadline_ns;
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -67,11 +69,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 // spin until *p >= want; false (error word raised) past the deadline
-__device__ bool spin_ge(const unsigned long long* p, unsigned long long want, int* err) {
+__device__ bool spin_ge(const unsigned long long* p, unsigned long long want, int* err,
+                        unsigned long long deadline_ns) {
   const unsigned long long t0 = global_ns();
   while (ld_acquire_sys(p) < want) {
     if (*(volatile int*)err) return false;   // another wait already failed: stop too
-    if (global_ns() - t0 > PEER_DEADLINE_NS) {
+    if (global_ns() - t0 > deadline_ns) {
       *(volatile int*)err = 1;
       __threadfence_system();
       return false;
@@ -89,7 +92,7 @@ __global__ void k_peer_allreduce(double* v, int count, PeerView pv, unsigned lon
   __threadfence_system();
   __syncthreads();
   if (tid < pv.world) st_release_sys(&pv.mb[tid]->ar_tag[par][me], epoch);
-  if (tid < pv.world) spin_ge(&pv.mb[me]->ar_tag[par][tid], epoch, pv.err);
+  if (tid < pv.world) spin_ge(&pv.mb[me]->ar_tag[par][tid], epoch, pv.err, pv.deadline_ns);
   __syncthreads();
   __threadfence_system();
   const Mailbox* own = pv.mb[me];
@@ -103,7 +106,7 @@ __global__ void k_peer_allreduce(double* v, int count, PeerView pv, unsigned lon
 // wait until every listed peer has pushed halo `epoch` into this rank's window
 __global__ void k_peer_wait(PeerView pv, int npeers, int p0, int p1, unsigned long long epoch) {
   const int t = threadIdx.x;
-  if (t < npeers) spin_ge(&pv.mb[pv.rank]->halo_tag[t == 0 ? p0 : p1], epoch, pv.err);
+  if (t < npeers) spin_ge(&pv.mb[pv.rank]->halo_tag[t == 0 ? p0 : p1], epoch, pv.err, pv.deadline_ns);
   __syncthreads();
 }
 
@@ -181,6 +184,9 @@ int svb_peer_create(int rank, int world, svb_peer** out) {
       g->view.rank = rank;
       g->view.world = world;
       g->view.err = err_dev;
+      // SPMVTUNE_PEER_DEADLINE_MS shortens the wait deadline (tests of the error path)
+      const char* dl = std::getenv("SPMVTUNE_PEER_DEADLINE_MS");
+      g->view.deadline_ns = dl ? (unsigned long long)std::atoll(dl) * 1000000ull : PEER_DEADLINE_NS;
       g->view.mb[rank] = g->own;
     } catch (...) {
       if (g->own) cudaFree(g->own);
