@@ -780,6 +780,12 @@ __global__ void __launch_bounds__(KB) k_gm_update_x(Gm G, int j, double* __restr
 // CG
 // ---------------------------------------------------------------------------
 enum { S_PQ = 3 };   // scal slot of the fused SpMV+dot result
+// 1.0 while x += alpha p is pending: the update pass only moves r (reads r,
+// q; writes r: 24 B/row) and the p pass, which reads p anyway, also moves x
+// (reads x, r, p; writes x, p: 40 B/row) — 64 instead of 72 B/row of vector
+// traffic per iteration.  The flag keeps the x update exactly once per
+// iteration when a converged batch's later p passes are no-ops.
+enum { S_XPEND = 4 };
 
 // r = b - tmp; p = r; rr = r.r
 __global__ void __launch_bounds__(KB) k_cg_restart(int64_t n, const double* __restrict__ b,
@@ -806,6 +812,7 @@ __global__ void __launch_bounds__(KB) k_cg_restart(int64_t n, const double* __re
   double tot;
   if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
     scal[S_RR] = tot;
+    scal[S_XPEND] = 0.0;   // a restart starts from the current x
     st->beta = sqrt(tot);
     st->nonfinite = bad(tot);
   }
@@ -869,9 +876,9 @@ __global__ void __launch_bounds__(KB) k_cg_pq(int64_t n, const double* __restric
   }
 }
 
-// x += alpha p; r -= alpha q; rr' = r.r; beta = rr'/rr; estimate
-__global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
-                                                  const double* __restrict__ p, const double* __restrict__ q,
+// r -= alpha q; rr' = r.r; beta = rr'/rr; estimate; x += alpha p pending
+// (applied by k_cg_p)
+__global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict__ r, const double* __restrict__ q,
                                                   double* scal, double bnorm, double* partials,
                                                   unsigned* counter, svb_krylov_status* st, CgCtl* ctl) {
   if (ctl != nullptr && ctl->done) return;
@@ -880,29 +887,27 @@ __global__ void __launch_bounds__(KB) k_cg_update(int64_t n, double* __restrict_
   for_pairs(
       n,
       [&](int64_t e) {
-        double2 xx = ld2(x + e), rr = ld2(r + e), pp = ld2(p + e), qq = ld2(q + e);
-        xx.x += alpha * pp.x;
-        xx.y += alpha * pp.y;
+        double2 rr = ld2(r + e), qq = ld2(q + e);
         rr.x -= alpha * qq.x;
         rr.y -= alpha * qq.y;
-        st2(x + e, xx);
         st2(r + e, rr);
         acc += rr.x * rr.x;
         acc += rr.y * rr.y;
       },
       [&](int64_t e) {
-        x[e] += alpha * p[e];
         double rr = r[e] - alpha * q[e];
         r[e] = rr;
         acc += rr * rr;
       });
   double tot;
-  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) cg_after_update(scal, tot, bnorm, st, ctl);
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    scal[S_XPEND] = 1.0;
+    cg_after_update(scal, tot, bnorm, st, ctl);
+  }
 }
 
-// p = r + beta p
-__global__ void __launch_bounds__(KB) k_cg_update_pq(int64_t n, double* __restrict__ x, double* __restrict__ r,
-                                                     const double* __restrict__ p, const double* __restrict__ q,
+// the same with alpha = rr / (p.q) from the fused DIA SpMV+dot
+__global__ void __launch_bounds__(KB) k_cg_update_pq(int64_t n, double* __restrict__ r, const double* __restrict__ q,
                                                      double* scal, double bnorm, double* partials,
                                                      unsigned* counter, svb_krylov_status* st, CgCtl* ctl) {
   if (ctl->done) return;
@@ -922,37 +927,63 @@ __global__ void __launch_bounds__(KB) k_cg_update_pq(int64_t n, double* __restri
   for_pairs(
       n,
       [&](int64_t e) {
-        double2 xx = ld2(x + e), rr = ld2(r + e), pp = ld2(p + e), qq = ld2(q + e);
-        xx.x += alpha * pp.x;
-        xx.y += alpha * pp.y;
+        double2 rr = ld2(r + e), qq = ld2(q + e);
         rr.x -= alpha * qq.x;
         rr.y -= alpha * qq.y;
-        st2(x + e, xx);
         st2(r + e, rr);
         acc += rr.x * rr.x;
         acc += rr.y * rr.y;
       },
       [&](int64_t e) {
-        x[e] += alpha * p[e];
         double rr = r[e] - alpha * q[e];
         r[e] = rr;
         acc += rr * rr;
       });
   double tot;
-  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) cg_after_update(scal, tot, bnorm, st, ctl);
+  if (grid_sum_last(acc, partials, counter, &tot) && threadIdx.x == 0) {
+    scal[S_ALPHA] = alpha;
+    scal[S_XPEND] = 1.0;
+    cg_after_update(scal, tot, bnorm, st, ctl);
+  }
 }
 
-__global__ void __launch_bounds__(KB) k_cg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
-                                             const double* scal, const CgCtl* ctl) {
-  if (ctl != nullptr && ctl->done) return;
-  const double beta = scal[S_BETA];
+// x += alpha p (when pending: once per update, even in the iteration that
+// converged), then p = r + beta p unless the batch is done.  The last CTA
+// to finish clears the pending flag (every CTA read it at its start).
+__global__ void __launch_bounds__(KB) k_cg_p(int64_t n, double* __restrict__ x, const double* __restrict__ r,
+                                             double* __restrict__ p, double* scal, const CgCtl* ctl,
+                                             unsigned* counter) {
+  const bool xmove = scal[S_XPEND] != 0.0;
+  const bool pmove = !(ctl != nullptr && ctl->done);
+  if (!xmove && !pmove) return;
+  const double alpha = scal[S_ALPHA], beta = scal[S_BETA];
   for_pairs(
       n,
       [&](int64_t e) {
-        double2 rr = ld2(r + e), pp = ld2(p + e);
-        st2(p + e, make_double2(rr.x + beta * pp.x, rr.y + beta * pp.y));
+        const double2 pp = ld2(p + e);
+        if (xmove) {
+          const double2 xx = ld2(x + e);
+          st2(x + e, make_double2(xx.x + alpha * pp.x, xx.y + alpha * pp.y));
+        }
+        if (pmove) {
+          const double2 rr = ld2(r + e);
+          st2(p + e, make_double2(rr.x + beta * pp.x, rr.y + beta * pp.y));
+        }
       },
-      [&](int64_t e) { p[e] = r[e] + beta * p[e]; });
+      [&](int64_t e) {
+        const double pe = p[e];
+        if (xmove) x[e] = x[e] + alpha * pe;
+        if (pmove) p[e] = r[e] + beta * pe;
+      });
+  if (!xmove) return;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    scal[S_XPEND] = 0.0;
+    *counter = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1243,6 +1274,7 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
     k->g = alloc((mm + 1) * 8, s);
     k->y = alloc(mm * 8, s);
     k->scal = alloc(8 * 8, s);
+    SVB_CUDA_TRY(cudaMemsetAsync(k->scal->ptr, 0, 8 * 8, s));   // S_XPEND = 0
     k->partials = alloc(k->rgrid * 8, s);
     k->counter = alloc(8, s);
     SVB_CUDA_TRY(cudaMemsetAsync(k->counter->ptr, 0, 8, s));
@@ -1499,10 +1531,11 @@ int svb_cg_step(svb_krylov* k, double bnorm, void* stream) {
     unsigned* C = ptr<unsigned>(k->counter);
     k_cg_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->scal), P, C,
                                      k->st_dev, nullptr);
-    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
-                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev, nullptr);
-    mark(k, s);  // status is final here; the p update overlaps the host
-    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal), nullptr);
+    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->q), ptr<double>(k->scal), bnorm, P,
+                                         C, k->st_dev, nullptr);
+    mark(k, s);  // status is final here; the x/p pass overlaps the host
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
+                                    ptr<double>(k->scal), nullptr, C);
     note_launches(2);
     SVB_CHECK_LAUNCH();
   });
@@ -1547,9 +1580,10 @@ int svb_cg_step_batched(svb_krylov* k, double bnorm, void* stream) {
     CgCtl* ctl = ptr<CgCtl>(k->ctl);
     k_cg_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->scal), P, C,
                                      k->st_dev, ctl);
-    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
-                                         ptr<double>(k->q), ptr<double>(k->scal), bnorm, P, C, k->st_dev, ctl);
-    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), ptr<double>(k->scal), ctl);
+    k_cg_update<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->q), ptr<double>(k->scal), bnorm, P,
+                                         C, k->st_dev, ctl);
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
+                                    ptr<double>(k->scal), ctl, C);
     note_launches(2);
     SVB_CHECK_LAUNCH();
     mark(k, s);
@@ -1575,10 +1609,10 @@ int svb_cg_step_batched_dia(svb_krylov* k, const svb_matrix* m, double bnorm, vo
     launch_dia_dot(m, ptr<double>(k->p), ptr<double>(k->q), ptr<double>(k->p), ptr<double>(k->dparts),
                    reinterpret_cast<unsigned*>(ptr<double>(k->dparts) + k->dgrid), sc + S_PQ, &ctl->done,
                    k->dgrid, s);
-    k_cg_update_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p),
-                                            ptr<double>(k->q), sc, bnorm, P, C, k->st_dev, ctl);
+    k_cg_update_pq<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->q), sc, bnorm, P, C, k->st_dev,
+                                            ctl);
     SVB_CHECK_LAUNCH();
-    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->r), ptr<double>(k->p), sc, ctl);
+    k_cg_p<<<k->rgrid, KB, 0, s>>>(k->n, ptr<double>(k->x), ptr<double>(k->r), ptr<double>(k->p), sc, ctl, C);
     SVB_CHECK_LAUNCH();
     mark(k, s);
   });
