@@ -618,6 +618,7 @@ def _timed(fn, reps=3):
         ts.append(time.perf_counter() - t0)
         if hasattr(rep, "solution"):
             rep.solution = None
+    _timed.last = [round(t, 6) for t in ts]       # every rep, so slow outliers stay visible
     return statistics.median(ts), rep
 
 
@@ -731,9 +732,11 @@ def config1_detail(args, P, device, _lib, models) -> dict:
         P.async_solve(A, b, params, models, method="cg", initial_config=start).solution = None
         out["async_s"], r = _timed(lambda: P.async_solve(A, b, params, models, method="cg",
                                                          initial_config=start), reps=5)
+        out["async_reps_s"] = _timed.last
         out.update({"iterations": r.iterations, "converged": r.converged, "final_residual": r.final_residual,
                     "swaps": [(x.iteration, x.config.token()) for x in r.config_timeline]})
         out["default_csr_vector_s"], d = _timed(lambda: P.cg_solve(A, b, params, initial_config=start), reps=3)
+        out["default_reps_s"] = _timed.last
         out["default_iterations"] = d.iterations
     return out
 
