@@ -38,6 +38,8 @@ struct svb_matrix {
   mutable int64_t ntiles = -1;
   mutable int tile_cap = 0;  // entry capacity the tiles were cut for
   mutable svb::Buf tiles;
+  // the row kernel's dynamic tile counters, one per launching stream
+  mutable std::vector<std::pair<cudaStream_t, svb::Buf>> tctr;
   // COO: row-run starts (int64 row pointer derived from the sorted rows —
   // what np.flatnonzero(np.diff(rows)) computes on every reference call)
   mutable svb::Buf dptr;

@@ -459,8 +459,10 @@ __device__ void cta_long_row(int row, int64_t s, int64_t e, const int* __restric
 
 // LANE: CSR/LibA/L lane tree; otherwise numpy pairwise (LibB, COO/LibA, HYB
 // spill) or chunk pieces (LibC, bounds != nullptr).
-template <class T, class P, bool ADD, bool LANE, int CAP, int NS>
-__global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, const RowTile* __restrict__ tiles,
+// Lane-tree variants with <= 1536-entry tiles fit 5 CTAs per SM when they
+// keep <= 96 registers (97 drops them to 4: config 2 CSR/LibA 96 -> 106 us).
+template <class T, class P, bool ADD, bool LANE, int CAP, int NS, bool DYN>
+__global__ void __launch_bounds__(ROWSEG_ROWS, (LANE && CAP <= 1536) ? 5 : 4) k_rows_pipe(int64_t ntiles, const RowTile* __restrict__ tiles,
                                                            const P* __restrict__ ptr, const int* __restrict__ cols,
                                                            const T* __restrict__ vals, const T* __restrict__ x,
                                                            T* __restrict__ y, const int64_t* __restrict__ bounds,
@@ -468,13 +470,15 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
                                                            const int* __restrict__ lrow,
                                                            const int64_t* __restrict__ lbeg,
                                                            const int64_t* __restrict__ lend,
-                                                           const int* __restrict__ rowmap) {
+                                                           const int* __restrict__ rowmap,
+                                                           unsigned long long* __restrict__ ctr) {
   using L = PipeLayout<T, P, CAP, NS>;
   constexpr int U = CAP / ROWSEG_ROWS;  // products per thread per tile (one round of gathers)
   static_assert(CAP % ROWSEG_ROWS == 0 && CAP >= MED_ROW, "tile capacity");
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ alignas(8) uint64_t bar[NS];
   __shared__ RowTile desc[NS];
+  __shared__ int64_t sidx[DYN ? NS : 1];   // DYN: tile index each stage holds (>= ntiles: none)
   __shared__ int smed[ROWSEG_ROWS];
   __shared__ int nmed;
   constexpr int NL = LANE ? 1 : MED_LEAVES;
@@ -493,10 +497,20 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
       __syncthreads();
     }
   }
+  // Tile order: !DYN (regular matrices) round robin, tiles
+  // blockIdx.x + k*gridDim.x; DYN (irregular matrices)
+  // every CTA claims the next unclaimed tiles once its long rows are done, so
+  // a CTA that spent its start on a long row, or whose tiles hold medium
+  // rows, takes fewer tiles — with the static order the slowest SM ran 1.6x
+  // the average on config 3's HYB spill.  ctr[0] counts claims, ctr[1]
+  // finished CTAs; the last CTA resets both, so the next launch on this
+  // stream needs no memset.
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    const int64_t first = DYN ? (int64_t)atomicAdd(ctr, (unsigned long long)NS) : 0;
     for (int s = 0; s < NS; ++s) {
-      const int64_t ti = blockIdx.x + (int64_t)s * gridDim.x;
+      const int64_t ti = DYN ? first + s : blockIdx.x + (int64_t)s * gridDim.x;
+      if constexpr (DYN) sidx[s] = ti;
       if (ti < ntiles) {
         desc[s] = tiles[ti];
         issue_tile<T, P, L>(ring + s * L::STAGE, &bar[s], desc[s], ptr, cols, vals, policy);
@@ -519,17 +533,21 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
       if (j < gn) xv[u] = ld_x(x + gsc[goff + j]);
     }
   };
-  if (blockIdx.x < ntiles) gather(0);
-  int it = 0;
-  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++it) {
+  // ti: the tile stage it % NS holds (stages are consumed in claim order)
+  int64_t ti = DYN ? sidx[0] : (int64_t)blockIdx.x;
+  if (ti < ntiles) gather(0);
+  for (int it = 0; ti < ntiles; ++it) {
     const int st = it % NS;
     unsigned char* stage = ring + st * L::STAGE;
     T* sv = reinterpret_cast<T*>(stage);
     const P* sp = reinterpret_cast<const P*>(stage + L::SV + L::SC);
-    // descriptor of the tile this stage takes next, fetched early
-    const int64_t tn = ti + (int64_t)NS * gridDim.x;
+    // claim the tile this stage takes next, descriptor fetched early
+    int64_t tn = ntiles;
     RowTile nxt{};
-    if (tid == 0 && tn < ntiles) nxt = tiles[tn];
+    if (tid == 0) {
+      tn = DYN ? (int64_t)atomicAdd(ctr, 1ull) : ti + (int64_t)NS * gridDim.x;
+      if (tn < ntiles) nxt = tiles[tn];
+    }
     const RowTile t = desc[st];
     const int64_t pa = t.r0 & ~(int64_t)(L::PQ - 1);
     const int64_t A0 = t.e0 & ~int64_t(3);
@@ -541,7 +559,9 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
       if (j < n) sv[off + j] = sv[off + j] * xv[u];
     }
     __syncthreads();
-    if (ti + gridDim.x < ntiles) {
+    // the next stage's claim was written at least one barrier ago
+    const int64_t tnext = DYN ? sidx[(it + 1) % NS] : ti + gridDim.x;
+    if (tnext < ntiles) {
       gather_it = it + 1;
       gather((it + 1) % NS);
     }
@@ -581,10 +601,21 @@ __global__ void __launch_bounds__(ROWSEG_ROWS, 4) k_rows_pipe(int64_t ntiles, co
       }
     }
     __syncthreads();  // stage st and the medium-row list are free again
-    if (tid == 0 && tn < ntiles) {
-      fence_proxy_async_smem();
-      desc[st] = nxt;
-      issue_tile<T, P, L>(stage, &bar[st], nxt, ptr, cols, vals, policy);
+    if (tid == 0) {
+      if constexpr (DYN) sidx[st] = tn;
+      if (tn < ntiles) {
+        fence_proxy_async_smem();
+        desc[st] = nxt;
+        issue_tile<T, P, L>(stage, &bar[st], nxt, ptr, cols, vals, policy);
+      }
+    }
+    ti = tnext;
+  }
+  if (DYN && tid == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
     }
   }
 }
@@ -1296,28 +1327,60 @@ static int64_t tile_list(const svb_matrix* m, const P* rp, int cap, cudaStream_t
   return total;
 }
 
+// Per-(handle, stream) counters of the row kernel's dynamic tile scheduler
+// (zeroed once here, reset by the last CTA of every launch; launches on one
+// stream are serialised, so they never share a live counter).
+static unsigned long long* tile_counter(const svb_matrix* m, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  for (auto& e : m->tctr)
+    if (e.first == s) return ptr<unsigned long long>(e.second);
+  Buf b = alloc(16, s);
+  SVB_CUDA_TRY(cudaMemsetAsync(b->ptr, 0, 16, s));
+  detach(b);
+  m->tctr.emplace_back(s, b);
+  return ptr<unsigned long long>(b);
+}
+
+template <class T, class P, bool ADD, bool LANE, int CAP, int NS, bool DYN>
+static void launch_rows_kernel(const svb_matrix* m, int64_t nt, int64_t nl, const P* rp, const int* cols,
+                               const T* vals, const T* x, T* y, const int64_t* bounds, int nb, int lanes,
+                               cudaStream_t s) {
+  using L = PipeLayout<T, P, CAP, NS>;
+  auto* kern = k_rows_pipe<T, P, ADD, LANE, CAP, NS, DYN>;
+  static const int occ = [kern] {
+    SVB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES));
+    int o = 0;
+    SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, ROWSEG_ROWS, L::BYTES));
+    return o < 1 ? 1 : o;
+  }();
+  const int64_t work = nt > nl ? nt : nl;
+  const int64_t cap = (int64_t)sm_count() * occ;
+  const unsigned g = (unsigned)(work < cap ? work : cap);
+  kern<<<g, ROWSEG_ROWS, L::BYTES, s>>>(nt, ptr<RowTile>(m->tiles), rp, cols, vals, x, y, bounds, nb, lanes, nl,
+                                        ptr<int>(m->lrow), ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend),
+                                        m->fmt == SVB_HYB ? ptr<int>(m->hmap) : nullptr,
+                                        DYN ? tile_counter(m, s) : nullptr);
+  SVB_CHECK_LAUNCH();
+}
+
 template <class T, class P, bool ADD, bool LANE, int CAP, int NS>
 static void launch_rows_cfg(const svb_matrix* m, const P* rp, const int* cols, const T* vals, const T* x, T* y,
                             const int64_t* bounds, int nb, int lanes, cudaStream_t s) {
-  using L = PipeLayout<T, P, CAP, NS>;
   const int64_t nt = tile_list(m, rp, CAP, s);
   const int64_t nl = long_list(m, s);
-  const int64_t work = nt > nl ? nt : nl;
-  if (work <= 0) return;
-  static const int occ = [] {
-    SVB_CUDA_TRY(cudaFuncSetAttribute(k_rows_pipe<T, P, ADD, LANE, CAP, NS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES));
-    int o = 0;
-    SVB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_rows_pipe<T, P, ADD, LANE, CAP, NS>,
-                                                               ROWSEG_ROWS, L::BYTES));
-    return o < 1 ? 1 : o;
+  if ((nt > nl ? nt : nl) <= 0) return;
+  // dynamic tile claims where per-tile work varies: rows longer than
+  // MED_ROW exist; the round-robin order stays for regular matrices, where
+  // the shared counter cost 2-9 us per launch on configs 1/2
+  // (SPMVTUNE_ROWDYN=0/1 forces either order for experiments)
+  static const int dyn_env = [] {
+    const char* e = getenv("SPMVTUNE_ROWDYN");
+    return e ? atoi(e) : -1;
   }();
-  const int64_t cap = (int64_t)sm_count() * occ;
-  const unsigned g = (unsigned)(work < cap ? work : cap);
-  k_rows_pipe<T, P, ADD, LANE, CAP, NS><<<g, ROWSEG_ROWS, L::BYTES, s>>>(
-      nt, ptr<RowTile>(m->tiles), rp, cols, vals, x, y, bounds, nb, lanes, nl, ptr<int>(m->lrow),
-      ptr<int64_t>(m->lbeg), ptr<int64_t>(m->lend), m->fmt == SVB_HYB ? ptr<int>(m->hmap) : nullptr);
-  SVB_CHECK_LAUNCH();
+  if (dyn_env >= 0 ? dyn_env > 0 : nl > 0)
+    launch_rows_kernel<T, P, ADD, LANE, CAP, NS, true>(m, nt, nl, rp, cols, vals, x, y, bounds, nb, lanes, s);
+  else
+    launch_rows_kernel<T, P, ADD, LANE, CAP, NS, false>(m, nt, nl, rp, cols, vals, x, y, bounds, nb, lanes, s);
 }
 
 // The persistent row kernel.  The tile capacity follows the mean entries per

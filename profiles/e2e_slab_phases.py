@@ -30,7 +30,24 @@ offs, w = bench.stencil27()
 blk = stencil_block(dims, offs, w, 0, n3 ** 3, device.thread_stream(0))
 models = P.CascadeModelSet.load_dir(ROOT / "tests" / "golden" / "models")
 params = P.GmresParams(tol=1e-8, max_iters=20000)
-args = argparse.Namespace(steps=4, e2e_steps=4)
+k = int(os.environ.get("SPMVTUNE_E2E_STEPS", "4"))
+args = argparse.Namespace(steps=k, e2e_steps=k)
+import paper_2411_10143_b200.distributed as D  # noqa: E402
+_solve = D.distributed_solve_slab
+
+
+def traced(*a, **kw):                    # pool state around every solve (fragmentation check)
+    i0 = device.device_info()
+    r = _solve(*a, **kw)
+    i1 = device.device_info()
+    t = kw.get("timings")
+    if t is not None:
+        t["pool_gb"] = [round(i0["pool_reserved_bytes"] / 1e9, 2), round(i1["pool_reserved_bytes"] / 1e9, 2),
+                        round(i1["free_bytes"] / 1e9, 2)]
+    return r
+
+
+D.distributed_solve_slab = traced
 out = bench.e2e_slab(args, blk, 0, n3 ** 3, params, models, None, 1)
 print(json.dumps({"value": out["value"], "phases": out["phases"]}))
 dist.destroy_process_group()
