@@ -79,6 +79,43 @@ def test_larger_matrices_against_oracle(gen):
     assert rel(got, O.spmv_sequential(ocsr, x)) <= 1e-12
 
 
+def _skewed_csr(n=40000, seed=5):
+    """Short rows, medium rows (warp path) and rows longer than MED_ROW (whole
+    CTA): the row kernel then claims its tiles from the dynamic counter."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 20, size=n)
+    lens[rng.choice(n, 40, replace=False)] = rng.integers(129, 1024, size=40)
+    lens[rng.choice(n, 6, replace=False)] = [1025, 1500, 2049, 3000, 4100, 9000]
+    ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    cols = np.concatenate([np.sort(rng.choice(n, int(k), replace=False)) for k in lens]).astype(np.int64)
+    vals = rng.uniform(-1.0, 1.0, size=cols.size)
+    return n, n, ptr, cols, vals
+
+
+def test_dynamic_tile_claims_bit_exact_and_reset_across_launches_and_streams():
+    """Matrices with rows > MED_ROW run the row kernel with dynamic tile
+    claims (csrc/spmv.cu k_rows_pipe<..., DYN>): every deterministic CSR/COO/
+    HYB configuration stays bit-identical to the oracle, launch after launch
+    and on two streams (the per-(handle, stream) counter resets itself)."""
+    n, m, ptr, cols, vals = _skewed_csr()
+    csr = P.CsrMatrix(n, m, ptr, cols, vals)
+    ocsr = O.OCsr(n, m, ptr, cols, vals)
+    reps = {"CSR": ocsr, "COO": O.csr_to_coo(ocsr), "HYB": O.convert(ocsr, "HYB")}
+    x = np.random.default_rng(3).uniform(-1.0, 1.0, size=m)
+    streams = [device.thread_stream(), device.Stream(0)]
+    xds = [device.DeviceVector.from_numpy(x, s) for s in streams]
+    for cfg in P.enumerate_configs():
+        if cfg.format.value not in reps or cfg == ATOMIC:
+            continue
+        rep = P.convert(csr, cfg.format)
+        want = O.spmv(cfg.token(), reps[cfg.format.value], x, workers=4)
+        for k in range(6):
+            s = streams[k % 2]
+            got = P.execute_spmv(cfg, rep, xds[k % 2], workers=4, stream=s).to_numpy(s)
+            assert np.array_equal(got, want), (cfg.token(), k)
+
+
 FP32_TOL = 1e-5   # fp32 SpMV vs the fp64 result, relative 2-norm (fp32 values, x and sums)
 
 
