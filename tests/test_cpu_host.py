@@ -217,3 +217,21 @@ def test_native_mailbox_and_driver_argument_checks_on_host():
     with pytest.raises(ValueError):
         P.native_solve("bicgstab", None)
     del mb
+
+
+def test_native_loop_eligibility():
+    """Stock executors run the C++ solver loop; probes, plugin executors and
+    device-kept solutions keep the Python loop (solver._native_eligible)."""
+    from paper_2411_10143_b200 import solver as S
+    ex = S.SpmvExecutor.__new__(S.SpmvExecutor)
+    p = S.GmresParams()
+    assert S._native_eligible(ex, None, p, None) == (S._LOOP == "native")
+    assert not S._native_eligible(ex, None, p, lambda it, c: None)
+
+    class Plugin(S.SpmvExecutor):
+        def matvec(self, x):
+            return x
+
+    assert not S._native_eligible(Plugin.__new__(Plugin), None, p, None)
+    with S.DeviceOptions(keep_solution_on_device=True):
+        assert not S._native_eligible(ex, None, p, None)

@@ -9,7 +9,10 @@ import pytest
 
 import oracle as O
 import paper_2411_10143_b200 as P
+from paper_2411_10143_b200.solver import ADVISOR_COMPLETED
 from paper_2411_10143_b200 import generators as G
+from paper_2411_10143_b200 import solver
+from paper_2411_10143_b200.inference import model_from_dict
 
 pytestmark = pytest.mark.gpu
 
@@ -30,11 +33,13 @@ CASES = [
 
 
 @pytest.mark.parametrize("method,gen,tok,restart", CASES)
-def test_native_driver_matches_python_driver(method, gen, tok, restart):
+def test_native_driver_matches_python_driver(method, gen, tok, restart, monkeypatch):
     n, A, Ao = _mat(gen())
     cfg = P.SpmvConfig.from_token(tok)
     params = P.GmresParams(restart_m=restart, tol=1e-8, max_iters=3000)
+    monkeypatch.setattr(solver, "_LOOP", "python")     # the public call on the Python loop
     ref = (P.gmres_solve if method == "gmres" else P.cg_solve)(A, None, params, initial_config=cfg)
+    monkeypatch.setattr(solver, "_LOOP", "native")
     got = P.native_solve(method, A, None, params, cfg)
     assert got.iterations == ref.iterations and got.converged and ref.converged
     assert got.residual_history == ref.residual_history          # bit-identical
@@ -124,3 +129,68 @@ def test_native_mailbox_publish_before_solve_swaps_at_iteration_2():
     assert [(s.iteration, s.config.token()) for s in got.config_timeline] == [(1, "CSR/LibB"), (2, "DIA/LibA")]
     ref = P.gmres_solve(A, None, P.GmresParams(tol=1e-8))
     assert got.converged and abs(got.iterations - ref.iterations) <= 1
+
+
+def _forced_cascade(fmt):
+    def stub(classes, pick):
+        return model_from_dict({"schema_version": 1, "feature_names": list(P.FEATURE_NAMES),
+                                "classes": classes,
+                                "trees": [[{"score": 1.0 if c == pick else 0.0}] for c in classes]})
+    return P.CascadeModelSet(
+        format_model=stub(["COO", "CSR", "ELL", "DIA", "HYB"], fmt),
+        coo_lib_model=stub(["LibA", "LibB"], "LibA"),
+        csr_lib_model=stub(["LibA", "LibB", "LibC"], "LibA"),
+        ell_lib_model=stub(["LibA", "LibC"], "LibA"),
+        csr_tpv_model=stub(["2", "4", "8", "16", "32"], "32"))
+
+
+@pytest.mark.parametrize("method", ["gmres", "cg"])
+def test_public_solves_run_the_native_loop(method, monkeypatch):
+    """gmres_solve / cg_solve / sequential_predict_solve / async_solve with
+    stock executors run the C++ loop (no GIL held while the advisor works);
+    each report is bit-identical to the same call on the Python loop, and the
+    async advisor's DIA publish reaches the native mailbox."""
+    n, A, Ao = _mat(G.poisson2d(120) if method == "cg" else G.convdiff9(120))
+    params = P.GmresParams(restart_m=30, tol=1e-8, max_iters=4000)
+    models = _forced_cascade("DIA")
+    fixed_fn = P.gmres_solve if method == "gmres" else P.cg_solve
+    calls = []
+    real = solver.native_solve
+    monkeypatch.setattr(solver, "native_solve", lambda *a, **k: calls.append(a[0]) or real(*a, **k))
+    fixed = fixed_fn(A, None, params)
+    seq = P.sequential_predict_solve(A, None, params, models, method=method)
+    asy = P.async_solve(A, None, params, models, method=method)
+    assert calls == [method] * 3
+    monkeypatch.setattr(solver, "_LOOP", "python")
+    fixed_py = fixed_fn(A, None, params)
+    seq_py = P.sequential_predict_solve(A, None, params, models, method=method)
+    assert calls == [method] * 3
+    for got, ref in ((fixed, fixed_py), (seq, seq_py)):
+        assert got.converged and got.iterations == ref.iterations
+        assert got.residual_history == ref.residual_history
+        assert np.array_equal(got.solution, ref.solution)
+    assert fixed.mode == "fixed" and seq.mode == "sequential" and asy.mode == "async"
+    assert seq.config_timeline[0].config.token() == "DIA/LibA"
+    toks = [s.config.token() for s in asy.config_timeline]
+    assert asy.converged and toks[0] == P.DEFAULT_CONFIG.token()
+    if len(toks) > 1:                      # the publish may land after convergence
+        assert toks[1:] == ["DIA/LibA"] and asy.config_timeline[1].iteration >= 2
+        assert asy.advisor_outcome == ADVISOR_COMPLETED
+    assert abs(asy.iterations - fixed.iterations) <= 1
+    assert np.linalg.norm(asy.solution - fixed.solution) <= 1e-6 * np.linalg.norm(fixed.solution)
+
+
+def test_probe_and_plugin_executor_keep_the_python_loop(monkeypatch):
+    n, A, _ = _mat(G.poisson2d(20))
+    calls = []
+    real = solver.native_solve
+    monkeypatch.setattr(solver, "native_solve", lambda *a, **k: calls.append(a[0]) or real(*a, **k))
+
+    class Plugin(P.SpmvExecutor):
+        def matvec(self, x):
+            return super().matvec(x)
+
+    seen = []
+    P.gmres_solve(A, None, P.GmresParams(tol=1e-8), matvec_probe=lambda it, c: seen.append(it))
+    P.gmres_solve(A, None, P.GmresParams(tol=1e-8), executor=Plugin(P.DEFAULT_CONFIG, P.to_coo(A)))
+    assert calls == [] and seen
