@@ -40,6 +40,8 @@ struct svb_krylov {
   // plan, tagged exchange slots and the per-launch epoch of the tags
   bool tma = false;
   int tma_chunks = 0, tma_stages = 0, tma_nres = 0;
+  int tma_grid = 0;          // CTAs of the TMA Arnoldi kernel (mgs_grid)
+  int64_t tma_chunk = 0;     // its slice length
   unsigned long long epoch = 0;
   svb::Buf gslot;
   // recorded right after every status-producing kernel: the host waits on
@@ -1248,6 +1250,19 @@ using namespace svb;
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// CTAs of the TMA Arnoldi kernel.  Every MGS pass ends in a grid-wide
+// exchange whose latency grows with the number of CTAs taking part, while a
+// small basis is L2-resident and cheap to stream from few SMs: small systems
+// run on fewer CTAs.  SPMVTUNE_MGS_GRID overrides (A/B runs).
+static int mgs_grid(int64_t n, int sms) {
+  if (const char* e = std::getenv("SPMVTUNE_MGS_GRID")) {
+    const int g = std::atoi(e);
+    if (g >= 1 && g <= sms)
+      return std::min<int>(sms, std::max<int>(g, (int)((n + svb::mgs::MAX_SLICE - 1) / svb::mgs::MAX_SLICE)));
+  }
+  return sms;
+}
+
 extern "C" {
 
 int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
@@ -1296,7 +1311,10 @@ int svb_krylov_create(int64_t n, int32_t m, svb_krylov** out) {
       // SMs) run partially resident up to n = 19.4 M (mgs::plan)
       const bool tma_ok = !(mode && (std::strcmp(mode, "resident") == 0 || std::strcmp(mode, "tmem") == 0)) &&
                           m + 2 < 255;
-      if (allowed && coop && m >= 1 && tma_ok && mgs::plan(k->chunk, &k->tma_chunks, &k->tma_stages, &k->tma_nres) &&
+      k->tma_grid = mgs_grid(n, G);
+      k->tma_chunk = (((n + k->tma_grid - 1) / k->tma_grid) + 1) & ~int64_t(1);
+      if (allowed && coop && m >= 1 && tma_ok &&
+          mgs::plan(k->tma_chunk, &k->tma_chunks, &k->tma_stages, &k->tma_nres) &&
           mgs::SMEM <= (size_t)optin) {
         const void* kern = k->tma_nres < k->tma_chunks ? (const void*)mgs::k_mgs_tma<true>
                                                        : (const void*)mgs::k_mgs_tma<false>;
@@ -1434,7 +1452,7 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
       A.V = G.V;
       A.n = G.n;
       A.ld = G.ld;
-      A.chunk = k->chunk;
+      A.chunk = k->tma_chunk;
       A.m = G.m;
       A.j = j;
       A.H = G.H;
@@ -1452,7 +1470,7 @@ int svb_gmres_arnoldi(svb_krylov* k, int32_t j, double bnorm, void* stream) {
       void* args[] = {&A};
       const void* kern = k->tma_nres < k->tma_chunks ? (const void*)mgs::k_mgs_tma<true>
                                                      : (const void*)mgs::k_mgs_tma<false>;
-      SVB_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(sm_count()), dim3(mgs::NT), args, mgs::SMEM, s));
+      SVB_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(k->tma_grid), dim3(mgs::NT), args, mgs::SMEM, s));
       note_launches(1);
       k->normalized = j;
       mark(k, s);
