@@ -1253,14 +1253,18 @@ static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // CTAs of the TMA Arnoldi kernel.  Every MGS pass ends in a grid-wide
 // exchange whose latency grows with the number of CTAs taking part, while a
 // small basis is L2-resident and cheap to stream from few SMs: small systems
-// run on fewer CTAs.  SPMVTUNE_MGS_GRID overrides (A/B runs).
+// run on fewer CTAs, one per 4096 rows (two ring chunks), at least 32.
+// Measured per GMRES(30) iteration (profiles/r2_mgs_grid_ab.json, G = 148 ->
+// this rule): n = 65 K 70.9 -> 50.3 us, 131 K 72.8 -> 57.7, 262 K 77.4 ->
+// 63.9; from n = 606 K on all 148 SMs take part as before.
+// SPMVTUNE_MGS_GRID overrides (A/B runs).
 static int mgs_grid(int64_t n, int sms) {
+  int g = (int)std::min<int64_t>(sms, std::max<int64_t>(32, (n + 4095) / 4096));
   if (const char* e = std::getenv("SPMVTUNE_MGS_GRID")) {
-    const int g = std::atoi(e);
-    if (g >= 1 && g <= sms)
-      return std::min<int>(sms, std::max<int>(g, (int)((n + svb::mgs::MAX_SLICE - 1) / svb::mgs::MAX_SLICE)));
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= sms) g = v;
   }
-  return sms;
+  return std::min<int>(sms, std::max<int>(g, (int)((n + svb::mgs::MAX_SLICE - 1) / svb::mgs::MAX_SLICE)));
 }
 
 extern "C" {
