@@ -66,6 +66,8 @@ def matrix(name: str):
         return G.laplace27(120)     # config 5's matrix family at 120^3 (600^3 has 5.8 B nnz)
     if name == "config2_8M":
         return G.convdiff9(2830)    # config 2's family above the on-chip Arnoldi capacity (4.85 M rows)
+    if name in ("convdiff_362", "convdiff_512"):
+        return G.convdiff9(int(name.split("_")[1]))   # config 2's family where the Arnoldi kernel runs on 32 / 64 CTAs
     raise KeyError(name)
 
 
@@ -109,8 +111,9 @@ def cg_oracle(csr, tok, b, tol=1e-8, max_iters=20000) -> dict:
 
 
 def build_gmres_only(name: str) -> dict:
-    """config2_8M: the matrix hash and the reference's GMRES(30) on DIA only
-    (the partially resident Arnoldi kernel's parity target)."""
+    """config2_8M / convdiff_362 / convdiff_512: the matrix hash and the
+    reference's GMRES(30) on DIA only (the parity targets of the partially
+    resident and the reduced-grid Arnoldi kernels)."""
     t0 = time.perf_counter()
     n, m, ptr, cols, vals = matrix(name)
     doc = {"n": int(n), "nnz": int(cols.size),
@@ -130,7 +133,7 @@ def build_gmres_only(name: str) -> dict:
 
 
 def build(name: str, models) -> dict:
-    if name == "config2_8M":
+    if name in ("config2_8M", "convdiff_362", "convdiff_512"):
         return build_gmres_only(name)
     t0 = time.perf_counter()
     n, m, ptr, cols, vals = matrix(name)

@@ -311,3 +311,40 @@ def test_config5_family_row_partitioned_cg_matches_reference():
         assert np.allclose(res["history"][:5], f["cg"]["history_head"], rtol=1e-9, atol=0)
     finally:
         dist.destroy_process_group()
+
+
+_GRID_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, {root!r})
+import paper_2411_10143_b200 as P
+from paper_2411_10143_b200 import generators as G
+n, m, ptr, cols, vals = G.convdiff9({nx})
+A = P.convert(P.CsrMatrix(n, m, ptr, cols, vals), P.FormatTag.DIA)
+r = P.gmres_solve(A, None, P.GmresParams(restart_m=30, tol=1e-8, max_iters=1000),
+                  initial_config=P.SpmvConfig(P.FormatTag.DIA, P.Library.LIB_A))
+print(json.dumps({{"iterations": r.iterations, "converged": r.converged, "final": r.final_residual,
+                  "head": r.residual_history[:5]}}))
+"""
+
+
+@pytest.mark.parametrize("name,nx", [("convdiff_362", 362), ("convdiff_512", 512)])
+def test_reduced_grid_arnoldi_matches_reference(name, nx):
+    """131 K / 262 K rows: the TMA Arnoldi kernel runs on 32 / 64 CTAs (one
+    per 4096 rows, csrc/krylov.cu mgs_grid) instead of one per SM.  Both
+    grids land on the reference's own GMRES(30) run (fixtures made with the
+    reference's gmres_solve on DIA): same iteration count within 1, final
+    residual and the first residual estimates to 1e-6 relative."""
+    f = fixtures()[name]["gmres30"]
+    for grid in (None, "148"):
+        env = dict(os.environ)
+        env.pop("SPMVTUNE_MGS", None)
+        env.pop("SPMVTUNE_MGS_GRID", None)
+        if grid:
+            env["SPMVTUNE_MGS_GRID"] = grid
+        out = subprocess.run([sys.executable, "-c", _GRID_SCRIPT.format(root=str(ROOT), nx=nx)], env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        assert r["converged"] and abs(r["iterations"] - f["iterations"]) <= 1, (grid, r, f)
+        assert abs(r["final"] - f["final_residual"]) <= 1e-6 * f["final_residual"], (grid, r, f)
+        assert np.allclose(r["head"], f["history_head"], rtol=1e-6, atol=0), (grid, r, f)
