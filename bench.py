@@ -173,7 +173,7 @@ def reference_arm(args):
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "extrapolated": True,
             "detail": detail}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -512,7 +512,7 @@ def b200_arm(args):
                            "l2": "inputs larger than L2 (47 GB DIA + 71.5 GB CSR per GPU at N=1, 126 MB L2)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk, "detail": detail}
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -769,6 +769,27 @@ def config3_detail(args, P, device, _lib, models) -> dict:
     return out
 
 
+_RESULT_OUT = None
+
+
+def _claim_stdout() -> None:
+    """Keep stdout for the one JSON line: whatever native libraries write to
+    fd 1 (NCCL prints its version banner there when NCCL_DEBUG is set) goes
+    to stderr.  Called in the process that measures, never before
+    self_launch (the ranks inherit fd 1)."""
+    global _RESULT_OUT
+    if _RESULT_OUT is None:
+        sys.stdout.flush()
+        _RESULT_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    out = _RESULT_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -785,6 +806,7 @@ def main(argv=None):
     if args.warmup < 0 or args.steps < 1 or args.gpus < 1:
         raise SystemExit("--steps >= 1, --warmup >= 0, --gpus >= 1")
     if args.impl == "reference":
+        _claim_stdout()
         reference_arm(args)
         return 0
     ws_env = os.environ.get("WORLD_SIZE")
@@ -792,6 +814,7 @@ def main(argv=None):
         return self_launch(args)
     if ws_env is not None and int(ws_env) != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws_env}: launch one rank per GPU")
+    _claim_stdout()
     b200_arm(args)
     return 0
 

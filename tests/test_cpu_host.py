@@ -235,3 +235,18 @@ def test_native_loop_eligibility():
     assert not S._native_eligible(Plugin.__new__(Plugin), None, p, None)
     with S.DeviceOptions(keep_solution_on_device=True):
         assert not S._native_eligible(ex, None, p, None)
+
+
+def test_bench_stdout_carries_only_the_json_line():
+    """bench.py's measuring process keeps fd 1 for its JSON line; native
+    writes to stdout (NCCL's version banner) and Python prints go to stderr."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = ("import os, sys\nsys.argv = ['bench.py']\nimport bench\nbench._claim_stdout()\n"
+            "print('python noise')\nos.write(1, b'native noise\\n')\nbench.emit({'metric': 'x', 'value': 1})\n")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       cwd=Path(__file__).resolve().parent.parent, timeout=120)
+    assert p.returncode == 0, p.stderr[-1000:]
+    assert p.stdout == '{"metric": "x", "value": 1}\n'
+    assert "native noise" in p.stderr and "python noise" in p.stderr
