@@ -114,6 +114,12 @@ int svb_free(void* ptr);
 int svb_host_alloc(int64_t bytes, void** out);     /* pinned host memory */
 int svb_host_free(void* ptr);
 int svb_copy(void* dst, const void* src, int64_t bytes, void* stream);  /* any direction, async */
+/* Host numpy buffer <-> device: device -> pageable host copies of >= 12 MB
+ * go through a pinned staging buffer drained by several host threads;
+ * everything else copies directly.  Blocking like cudaMemcpy from pageable
+ * memory: returns when `src` may be reused (to_device) or `dst` holds the
+ * data. */
+int svb_copy_host(void* dst, const void* src, int64_t bytes, int32_t to_device, void* stream);
 int svb_memset(void* dst, int value, int64_t bytes, void* stream);
 int svb_device_info(int32_t* sm_count, int64_t* free_bytes, int64_t* total_bytes);
 /* stream-ordered pool: bytes reserved from the driver / currently in use */

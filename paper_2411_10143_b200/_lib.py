@@ -82,6 +82,7 @@ _SIGS = {
     "svb_host_alloc": [_I64, _PP],
     "svb_host_free": [_P],
     "svb_copy": [_P, _P, _I64, _P],
+    "svb_copy_host": [_P, _P, _I64, _I32, _P],
     "svb_memset": [_P, C.c_int, _I64, _P],
     "svb_device_info": [C.POINTER(C.c_int32), _PI64, _PI64],
     "svb_pool_info": [_PI64, _PI64],

@@ -117,7 +117,7 @@ class DeviceVector:
     def from_numpy(cls, a: np.ndarray, stream: Stream | None = None) -> "DeviceVector":
         a = np.ascontiguousarray(a)
         v = cls(a.size, a.dtype)
-        copy(v.ptr, a.ctypes.data, v.nbytes, stream)
+        copy_host(v.ptr, a.ctypes.data, v.nbytes, True, stream)
         if stream is None:
             _lib.check(_lib.lib().svb_stream_sync(None))
         else:
@@ -126,7 +126,7 @@ class DeviceVector:
 
     def to_numpy(self, stream: Stream | None = None) -> np.ndarray:
         out = np.empty(self.n, self.dtype)
-        copy(out.ctypes.data, self.ptr, self.nbytes, stream)
+        copy_host(out.ctypes.data, self.ptr, self.nbytes, False, stream)
         _lib.check(_lib.lib().svb_stream_sync(stream.handle if stream else None))
         return out
 
@@ -143,6 +143,16 @@ def copy(dst: int, src: int, nbytes: int, stream: Stream | None = None) -> None:
     if int(nbytes) == 0:         # zero-length vectors (a rank without rows) have no pointer
         return
     _lib.check(_lib.lib().svb_copy(dst, src, int(nbytes), stream.handle if stream else None))
+
+
+def copy_host(dst: int, src: int, nbytes: int, to_device: bool, stream: Stream | None = None) -> None:
+    """Host (numpy) buffer <-> device, blocking: downloads of 12 MB and more
+    into pageable buffers go through the library's multi-threaded pinned
+    staging (svb_copy_host); everything else copies directly."""
+    if int(nbytes) == 0:
+        return
+    _lib.check(_lib.lib().svb_copy_host(dst, src, int(nbytes), 1 if to_device else 0,
+                                        stream.handle if stream else None))
 
 
 def memset(dst: int, value: int, nbytes: int, stream: Stream | None = None) -> None:
